@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Headline benchmark: MM iterations/s of the Welsch-MM registration hot path
+(reference solver.hpp:224-289) on BASELINE.json config 2 — a 316x316 =
+99,856-vertex height-field source against a warped, jittered, holed,
+outlier-polluted target, ~3,000-node deformation graph, FP64.
+
+One step = one accepted MM iteration (one IterationRecord): correspondence,
+Welsch weights + energy, normal-equation assembly, block-Jacobi PCG solve,
+rotation projection, Anderson combine (m=5) with its energy safeguard, and
+the deformation of the next iterate. The timed run is the reference's
+fixed-count single-stage idiom (acceptance_main.cpp:207-215): nu fixed at the
+derived values, eps = 1e-300, so exactly `steps` iterations are accepted.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun): config 2 does not shard, so every rank runs
+an independent replica ("replicas only"); value = iterations of all ranks /
+max-over-ranks device time.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MM iterations/s (100K-vertex source, config 2)"
+UNIT = "iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- distributed
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.torch, self.dist = torch, dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v):
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v):
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- workload
+def problem_for(config, rank=0):
+    from paper_2206_03410_b200 import registration as R
+    return R.make_problem(config)
+
+
+def pcg_bytes_per_iteration(N, P):
+    """one PCG iteration reads K once, the preconditioner and
+    six 12N vectors: 128 (N+P) + 128 N + 6 * 96 N bytes."""
+    return 128 * (N + P) + 128 * N + 6 * 96 * N
+
+
+def iteration_fixed_bytes(n, m, sumk, N, P, mk=5):
+    """SURVEY.md 8(d) fixed part of one MM iteration (without PCG)."""
+    kbar = sumk / n
+    per_vertex = (104 + 12 * kbar) * n
+    target = 16 * m
+    node = 128 * (N + P) + 96 * N + 4 * 96 * N + 16 * P
+    aa = (2 * mk + 4) * 96 * N
+    return per_vertex + target + node + aa
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def h2d_d2h_bytes(p):
+    g = p.graph
+    h2d = (p.source.nbytes + p.target.nbytes + g.node_positions.nbytes + 4 * g.edges.size +
+           4 * g.infl_offsets.size + 4 * g.infl_nodes.size + 8 * g.infl_weights.size + 4 * g.reg_pairs.size +
+           8 * g.reg_weights.size)
+    d2h = 96 * g.node_count + 24 * p.n
+    return int(h2d), int(d2h)
+
+
+def cpu_baseline(p, cfg_kw, warmup, steps):
+    from oracle import binding as O
+    cfg = O.config(**cfg_kw)
+    sec = O.time_iterations(p, cfg, warmup, steps)
+    return steps / sec, sec
+
+
+def run_reference(args, dist):
+    """The reference's own CPU implementation of the path: the unbuildable
+    Eigen reference is replaced by its restatement (oracle/), single thread
+    per registration as the reference (README.md:217-219)."""
+    if dist.rank != 0:
+        dist.barrier()
+        dist.close()
+        return
+    from oracle import binding as O
+    p = problem_for(args.config)
+    prm = O.init_parameters(p)
+    kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300)
+    steps = max(1, min(args.steps, 10))
+    warm = max(1, min(args.warmup, 3))
+    value, sec = cpu_baseline(p, kw, warm, steps)
+    g = p.graph
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * sec / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {p.n} source / {len(p.target)} target points, "
+                               f"{g.node_count} nodes, fixed-count single stage",
+                   "sample": f"{steps} MM iterations after {warm} warm-up"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{steps} MM iterations of config {args.config} after {warm} warm-up, "
+                                   "oracle restatement (reference needs Eigen, absent)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.close()
+
+
+def run_b200(args, dist):
+    from paper_2206_03410_b200 import registration as R
+
+    p = problem_for(args.config, dist.rank)
+    g = p.graph
+    n, m, N, P, sumk = p.n, len(p.target), g.node_count, g.pair_count, len(g.infl_nodes)
+    ctx = R.Context(device=dist.local)
+    ctx.set_problem(p)
+    prm = ctx.init_parameters()
+    cfg_kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300)
+    K, W = args.steps, max(3, args.warmup)
+    cfg = R.solver_config(i_max=W + K + 10, **cfg_kw)
+    ctx.enable_timing(True)
+    ctx.begin(cfg)
+    ctx.iterate(W, flush_l2=not args.no_flush)  # untimed warm-up
+    s0 = ctx.stats()
+    dist.barrier()
+    with ClockSampler(dist.local) as clocks:
+        acc, done, dev_ms = ctx.iterate(K, flush_l2=not args.no_flush)
+    dist.barrier()
+    s1 = ctx.stats()
+    X, v, rep = ctx.finish()
+    if acc != K:
+        raise RuntimeError(f"only {acc} of {K} iterations accepted")
+    max_ms = dist.max(dev_ms)
+    total_iters = dist.sum(float(acc))
+    value = total_iters / (max_ms / 1e3)
+    kms = {k: s1["kernel_ms"][k] - s0["kernel_ms"][k] for k in s1["kernel_ms"]}
+    pcg_iters = s1["pcg_iterations"] - s0["pcg_iterations"]
+    launches = s1["launches"] - s0["launches"]
+    dominant = max(kms, key=kms.get)
+    peak, peak_src = load_peaks()
+    # dominant kernel roofline (per launch)
+    if dominant == "pcg":
+        bytes_per_launch = (pcg_iters / K) * pcg_bytes_per_iteration(N, P)
+        avg_ms = kms["pcg"] / K
+    else:
+        bytes_per_launch = iteration_fixed_bytes(n, m, sumk, N, P) / 6
+        avg_ms = kms[dominant] / K
+    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
+    step_bytes = iteration_fixed_bytes(n, m, sumk, N, P) + (pcg_iters / K) * pcg_bytes_per_iteration(N, P)
+    step_gbs = step_bytes / ((dev_ms / K) / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "pcg_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # end-to-end through the C ABI with host buffers (uploads, index build,
+    # init_parameters, K iterations, downloads), wall clock around the call
+    e2e_ctx = R.Context(device=dist.local)
+    cfg_e2e = R.solver_config(i_max=K, **cfg_kw)
+    t0 = time.perf_counter()
+    e2e_ctx.register(cfg_e2e, one_shot_problem=p)
+    e2e_s = time.perf_counter() - t0
+    e2e_iters = e2e_ctx.report()["total_iterations"]
+    e2e_ctx.close()
+    e2e_value = dist.sum(float(e2e_iters)) / dist.max(e2e_s)
+    h2d, d2h = h2d_d2h_bytes(p)
+
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cps, sec = cpu_baseline(p, cfg_kw, 1, args.cpu_steps)
+        cpu = {"value": cps, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_steps} MM iterations of config {args.config} (n={n}) after 1 warm-up, "
+                         "oracle restatement, one thread (the reference is single-threaded)"}
+    ctx.close()
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K, "warmup": W,
+            "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {args.config}: {n} source / {m} target points, {N} nodes, "
+                                   f"{P} directed pairs, sum k {sumk}, fixed-count single stage (nu fixed, "
+                                   "eps=1e-300), AA m=5",
+                       "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "1 GPU",
+                       "l2": "flushed (2x L2 write) before every timed iteration, outside the timed interval"
+                       if not args.no_flush else "not flushed (working set < L2)"},
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms},
+            "step_roofline": {"achieved": step_gbs, "frac": step_gbs / peak, "bytes_per_step": step_bytes},
+            "kernel_ms_per_step": {k: v / K for k, v in kms.items()},
+            "pcg_iterations_per_step": pcg_iters / K,
+            "nn_queries_per_s": n / (kms["nn"] / K / 1e3) if kms["nn"] > 0 else None,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "iterations": e2e_iters, "seconds": e2e_s},
+            "gpu_launches": launches,
+            "clocks": clocks.result(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    if args.impl == "reference":
+        run_reference(args, dist)
+    else:
+        run_b200(args, dist)
+
+
+if __name__ == "__main__":
+    main()

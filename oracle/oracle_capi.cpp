@@ -362,6 +362,46 @@ int oracle_register(const oracle_problem_view* p, const oracle_solver_config* c,
     });
 }
 
+namespace {
+struct Stopwatch : PassObserver {
+    int accepted = 0, warmup = 0, steps = 0;
+    std::chrono::steady_clock::time_point t_begin, t_end;
+    bool started = false, stopped = false;
+    void on_pass(int, int, const Correspondences&, const EnergyBreakdown&, bool reverted) override {
+        // a pass is observed before it is solved: the interval from the pass
+        // that starts iteration `warmup` to the pass that starts iteration
+        // `warmup + steps` covers exactly `steps` accepted iterations
+        if (reverted) return;
+        if (accepted == warmup && !started) {
+            started = true;
+            t_begin = std::chrono::steady_clock::now();
+        }
+        if (accepted == warmup + steps && !stopped) {
+            stopped = true;
+            t_end = std::chrono::steady_clock::now();
+        }
+        ++accepted;
+    }
+};
+}  // namespace
+
+int oracle_time_iterations(const oracle_problem_view* p, const oracle_solver_config* c, int32_t warmup,
+                           int32_t steps, double* seconds) {
+    return guard([&] {
+        const DeformationGraph g = graph_from_view(p);
+        const auto src = to_vec3(p->source, p->n);
+        const auto tgt = to_vec3(p->target, p->m);
+        SolverConfig cfg = config_from(c);
+        cfg.i_max = warmup + steps + 1;  // one extra pass closes the timed interval
+        Stopwatch sw;
+        sw.warmup = warmup;
+        sw.steps = steps;
+        register_surfaces(src, p->src_avg_edge_length, tgt, g, cfg, &sw);
+        if (!sw.stopped) throw NumericalError("oracle_time_iterations: run ended before the timed iterations");
+        *seconds = std::chrono::duration<double>(sw.t_end - sw.t_begin).count();
+    });
+}
+
 int oracle_init_parameters(const oracle_problem_view* p, const oracle_solver_config* c, double* out6) {
     return guard([&] {
         const DeformationGraph g = graph_from_view(p);

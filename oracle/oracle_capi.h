@@ -104,6 +104,11 @@ int oracle_register(const oracle_problem_view* p, const oracle_solver_config* cf
                     int32_t pass_cap, int32_t* pass_nn_index /* pass_cap*n or NULL */,
                     oracle_report_summary* summary);
 
+/* CPU baseline: wall time of `steps` accepted MM iterations after `warmup`
+ * accepted ones, single stage at the given config (fixed-count idiom). */
+int oracle_time_iterations(const oracle_problem_view* p, const oracle_solver_config* cfg, int32_t warmup,
+                           int32_t steps, double* seconds);
+
 /* init_parameters (solver.hpp:86-106): out6 = {nu_a, nu_r, nu_a_min, alpha, beta, forced_zero} */
 int oracle_init_parameters(const oracle_problem_view* p, const oracle_solver_config* cfg,
                            double* out6);

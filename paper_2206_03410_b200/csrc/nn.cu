@@ -1,0 +1,271 @@
+// Closest-point correspondence (reference SpatialIndex, kd_tree.hpp:17-107,
+// and find_correspondences, energy.hpp:28-42) on sm_100a.
+//
+// Index: targets sorted by 30-bit Morton code, grouped 8 per leaf, with an
+// implicit 8-ary tree of FP32 AABBs above the leaves (level l node k covers
+// level l-1 nodes 8k..8k+7). Points are stored once as float4 (x, y, z
+// relative to the index centre, w = original index bits) so a leaf is two
+// coalesced 128-byte lines.
+//
+// Query: one 8-lane group per query (4 queries per warp). At an internal node
+// the 8 lanes test the 8 child boxes in parallel and push the survivors
+// nearest-last onto a per-group shared-memory stack; at a leaf the 8 lanes
+// test the 8 points. FP32 distances only prune: a candidate whose FP32
+// distance is within the rounding margin `delta` of the FP64 best is re-ranked
+// in FP64 from the original coordinates with the reference's tie rule
+// (d2 < best or d2 == best and index < best index, kd_tree.hpp:88). Boxes are
+// pruned only when their FP32 distance exceeds best + delta, i.e. never when
+// an equal-distance point could sit inside (the reference's non-strict prune,
+// kd_tree.hpp:99-100). The result is the exact FP64 argmin with the smallest
+// index on ties. The previous pass's index seeds the bound (warm start).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#include "device_common.cuh"
+#include "nn.cuh"
+
+namespace nrr_b200 {
+
+namespace {
+inline uint32_t spread10(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+}  // namespace
+
+void BvhHost::build(const double* tgt, int m_) {
+    m = m_;
+    if (m <= 0) throw NumericalError("SpatialIndex: cannot index an empty point set");
+    double lo[3] = {tgt[0], tgt[1], tgt[2]}, hi[3] = {tgt[0], tgt[1], tgt[2]};
+    for (int i = 1; i < m; ++i)
+        for (int c = 0; c < 3; ++c) {
+            const double v = tgt[3 * i + c];
+            if (!std::isfinite(v)) throw NumericalError("SpatialIndex: non-finite target point");
+            lo[c] = std::min(lo[c], v);
+            hi[c] = std::max(hi[c], v);
+        }
+    for (int c = 0; c < 3; ++c) center[c] = 0.5 * (lo[c] + hi[c]);
+    double ext = 0;
+    for (int c = 0; c < 3; ++c) ext = std::max(ext, hi[c] - lo[c]);
+    half_extent = 0;
+    std::vector<std::pair<uint32_t, int>> keys(m);
+    for (int i = 0; i < m; ++i) {
+        uint32_t code = 0;
+        for (int c = 0; c < 3; ++c) {
+            const double u = ext > 0 ? (tgt[3 * i + c] - lo[c]) / ext : 0.0;
+            const uint32_t q = static_cast<uint32_t>(std::min(1023.0, std::max(0.0, u * 1024.0)));
+            code |= spread10(q) << c;
+            half_extent = std::max(half_extent, std::abs(tgt[3 * i + c] - center[c]));
+        }
+        keys[i] = {code, i};
+    }
+    std::sort(keys.begin(), keys.end());
+    const int mpad = (m + 7) / 8 * 8;
+    pts.assign(mpad, make_float4(1e18f, 1e18f, 1e18f, 0.f));
+    for (int k = 0; k < mpad; ++k) {
+        int idx = -1;
+        if (k < m) {
+            idx = keys[k].second;
+            pts[k].x = static_cast<float>(tgt[3 * idx] - center[0]);
+            pts[k].y = static_cast<float>(tgt[3 * idx + 1] - center[1]);
+            pts[k].z = static_cast<float>(tgt[3 * idx + 2] - center[2]);
+        }
+        std::memcpy(&pts[k].w, &idx, 4);
+    }
+    // level 0 boxes over the leaves, then 8-ary levels until <= 8 nodes
+    level_off.clear();
+    level_cnt.clear();
+    box_lo.clear();
+    box_hi.clear();
+    int cnt = mpad / 8;
+    level_off.push_back(0);
+    level_cnt.push_back(cnt);
+    for (int k = 0; k < cnt; ++k) {
+        float4 l = make_float4(INFINITY, INFINITY, INFINITY, 0), h = make_float4(-INFINITY, -INFINITY, -INFINITY, 0);
+        for (int t = 0; t < 8; ++t) {
+            const int p = 8 * k + t;
+            if (p >= m) break;
+            l.x = std::min(l.x, pts[p].x);
+            l.y = std::min(l.y, pts[p].y);
+            l.z = std::min(l.z, pts[p].z);
+            h.x = std::max(h.x, pts[p].x);
+            h.y = std::max(h.y, pts[p].y);
+            h.z = std::max(h.z, pts[p].z);
+        }
+        box_lo.push_back(l);
+        box_hi.push_back(h);
+    }
+    while (cnt > 8) {
+        const int prev_off = level_off.back(), prev_cnt = cnt;
+        cnt = (prev_cnt + 7) / 8;
+        level_off.push_back(static_cast<int>(box_lo.size()));
+        level_cnt.push_back(cnt);
+        for (int k = 0; k < cnt; ++k) {
+            float4 l = make_float4(INFINITY, INFINITY, INFINITY, 0), h = make_float4(-INFINITY, -INFINITY, -INFINITY, 0);
+            for (int t = 0; t < 8; ++t) {
+                const int c = 8 * k + t;
+                if (c >= prev_cnt) break;
+                const float4 cl = box_lo[prev_off + c], ch = box_hi[prev_off + c];
+                l.x = std::min(l.x, cl.x);
+                l.y = std::min(l.y, cl.y);
+                l.z = std::min(l.z, cl.z);
+                h.x = std::max(h.x, ch.x);
+                h.y = std::max(h.y, ch.y);
+                h.z = std::max(h.z, ch.z);
+            }
+            box_lo.push_back(l);
+            box_hi.push_back(h);
+        }
+    }
+    if (level_cnt.size() > static_cast<size_t>(kMaxLevels - 1))
+        throw NumericalError("SpatialIndex: target too large for the BVH level table");
+}
+
+namespace {
+
+constexpr int kGroupsPerBlock = 32;  // 256 threads
+constexpr int kStack = 96;
+
+__device__ __forceinline__ double exact_d2(const double* t, double qx, double qy, double qz) {
+    // (t - q).squaredNorm() as x*x + y*y + z*z without contraction, as the
+    // reference / oracle evaluate it
+    const double dx = __dsub_rn(t[0], qx), dy = __dsub_rn(t[1], qy), dz = __dsub_rn(t[2], qz);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+__device__ __forceinline__ float box_dist(const float4& l, const float4& h, float qx, float qy, float qz) {
+    const float dx = fmaxf(fmaxf(l.x - qx, qx - h.x), 0.f);
+    const float dy = fmaxf(fmaxf(l.y - qy, qy - h.y), 0.f);
+    const float dz = fmaxf(fmaxf(l.z - qz, qz - h.z), 0.f);
+    return sqrtf(dx * dx + dy * dy + dz * dz);
+}
+
+__global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __restrict__ queries, int nq,
+                                                  const int* __restrict__ prev_idx, int* __restrict__ out_idx,
+                                                  double* __restrict__ out_d2, double* __restrict__ out_q,
+                                                  const double* __restrict__ anchor) {
+    __shared__ int st_node[kGroupsPerBlock][kStack];
+    __shared__ float st_dist[kGroupsPerBlock][kStack];
+    const int lane = threadIdx.x & 7;
+    const int gl = threadIdx.x >> 3;
+    const int group = blockIdx.x * kGroupsPerBlock + gl;
+    if (group >= nq) return;  // whole 8-lane group leaves together
+    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+    const int gshift = threadIdx.x & 24;
+
+    const double qx = queries[3 * group], qy = queries[3 * group + 1], qz = queries[3 * group + 2];
+    const float fx = static_cast<float>(qx - bv.cx), fy = static_cast<float>(qy - bv.cy),
+                fz = static_cast<float>(qz - bv.cz);
+    // FP32 rounding margin (|d32 - d64| <= ~5e-7 (S + |q-c|), 8x slack)
+    const float qmag = fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz)));
+    const float delta = 4e-6f * (bv.half_extent + qmag) + 1e-30f;
+
+    double best_d2 = INFINITY;
+    int best_i = 0x7fffffff;
+    if (prev_idx) {
+        const int p = prev_idx[group];
+        if (p >= 0 && p < bv.m) {
+            best_d2 = exact_d2(bv.tgt64 + 3 * p, qx, qy, qz);
+            best_i = p;
+        }
+    }
+    int* sn = st_node[gl];
+    float* sd = st_dist[gl];
+    int sp = 0;
+    if (lane == 0) {
+        sn[0] = ((bv.levels) << 27);  // virtual root above the top level
+        sd[0] = 0.f;
+    }
+    sp = 1;
+    __syncwarp(gmask);
+    while (sp > 0) {
+        --sp;
+        const int code = sn[sp];
+        const float bdist = sd[sp];
+        __syncwarp(gmask);
+        const float thr = static_cast<float>(sqrt(best_d2)) * 1.000001f + delta;  // inf stays inf
+        if (bdist > thr) continue;
+        const int L = code >> 27, v = code & ((1 << 27) - 1);
+        if (L == 0) {
+            const float4 p = bv.pts[8 * v + lane];
+            int idx;
+            memcpy(&idx, &p.w, 4);
+            const float dx = p.x - fx, dy = p.y - fy, dz = p.z - fz;
+            const float d2f = dx * dx + dy * dy + dz * dz;
+            double my_d2 = INFINITY;
+            int my_i = 0x7fffffff;
+            if (idx >= 0 && d2f <= thr * thr) {
+                my_d2 = exact_d2(bv.tgt64 + 3 * idx, qx, qy, qz);
+                my_i = idx;
+            }
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(gmask, my_d2, o, 8);
+                const int oi = __shfl_xor_sync(gmask, my_i, o, 8);
+                if (od < my_d2 || (od == my_d2 && oi < my_i)) {
+                    my_d2 = od;
+                    my_i = oi;
+                }
+            }
+            if (my_d2 < best_d2 || (my_d2 == best_d2 && my_i < best_i)) {
+                best_d2 = my_d2;
+                best_i = my_i;
+            }
+        } else {
+            const int cl = L - 1;
+            const int c = 8 * v + lane;
+            const bool exists = c < bv.level_cnt[cl];
+            float bd = INFINITY;
+            if (exists) {
+                const int b = bv.level_off[cl] + c;
+                bd = box_dist(bv.box_lo[b], bv.box_hi[b], fx, fy, fz);
+            }
+            const bool valid = exists && bd <= thr;
+            const unsigned ball = (__ballot_sync(gmask, valid) >> gshift) & 0xFFu;
+            const int cnt = __popc(ball);
+            // rank in descending distance (farthest pushed first, so the
+            // nearest child is popped next); every lane takes part
+            int rank = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float oj = __shfl_sync(gmask, bd, j, 8);
+                if (((ball >> j) & 1u) && j != lane && (oj > bd || (oj == bd && j < lane))) ++rank;
+            }
+            if (valid && sp + rank < kStack) {
+                sn[sp + rank] = (cl << 27) | c;
+                sd[sp + rank] = bd;
+            }
+            sp = min(sp + cnt, kStack);
+            __syncwarp(gmask);
+        }
+    }
+    if (lane == 0) {
+        out_idx[group] = best_i;
+        out_d2[group] = best_d2;
+        if (out_q) {
+            const double* t = bv.tgt64 + 3 * best_i;
+            out_q[3 * group] = t[0] - anchor[3 * group];
+            out_q[3 * group + 1] = t[1] - anchor[3 * group + 1];
+            out_q[3 * group + 2] = t[2] - anchor[3 * group + 2];
+        }
+    }
+}
+
+}  // namespace
+
+void launch_nn(const BvhView& bv, const double* queries, int nq, const int* prev_idx, int* out_idx, double* out_d2,
+               double* out_q, const double* anchor, cudaStream_t s) {
+    if (nq <= 0) return;
+    const int blocks = (nq + kGroupsPerBlock - 1) / kGroupsPerBlock;
+    nn_kernel<<<blocks, kGroupsPerBlock * 8, 0, s>>>(bv, queries, nq, prev_idx, out_idx, out_d2, out_q, anchor);
+    NRR_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace nrr_b200

@@ -1,0 +1,1120 @@
+// Host runtime of the B200 hot path: the device context (nrr_ctx) and the
+// register_surfaces state machine (reference solver.hpp:180-304) driving the
+// sm_100a kernels, plus the device entry points of the C ABI (nrr_cuda.h).
+//
+// Per accepted pass (one MM iteration) the stream runs:
+//   nn -> terms -> energy_reduce -> [host: accept/revert decision]
+//   -> assemble -> pcg (cooperative) -> aa_update -> aa_solve -> aa_combine
+//   -> deform(+max_disp) -> [host: record / convergence]
+// Two small pinned device->host copies per pass carry the energy record and
+// the solve status; all vectors stay resident in HBM.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device_common.cuh"
+#include "kernels.cuh"
+#include "nn.cuh"
+#include "nrr_cuda.h"
+#include "pcg.cuh"
+
+namespace nrr_b200 {
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void resize(size_t count) {
+        if (count == n && p) return;
+        release();
+        if (count == 0) return;
+        NRR_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        resize(count);
+        if (count) NRR_CUDA_CHECK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void zero(cudaStream_t s) {
+        if (n) NRR_CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+};
+
+template <typename T>
+struct Pinned {
+    T* p = nullptr;
+    Pinned() { NRR_CUDA_CHECK(cudaMallocHost(&p, sizeof(T))); }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+struct Params {  // SolverParams (solver.hpp:42-49)
+    double nu_a = 0, nu_r = 0, nu_a_min = 0, alpha = 0, beta = 0;
+    bool forced_zero = false;
+};
+
+// Sliding window of the reference's AndersonWindow (anderson.hpp:50-73),
+// vectors on the device, slot bookkeeping on the host.
+struct Window {
+    int m = 0;
+    int hist = 0;     // entries held (<= m+1)
+    int newest = -1;  // ring slot of the newest difference column
+    std::vector<int> cols;  // slots, newest first
+    void reset() {
+        hist = 0;
+        newest = m > 0 ? m - 1 : -1;
+        cols.clear();
+    }
+    bool extrapolating() const { return m > 0 && hist > 1; }  // anderson.hpp:64
+};
+
+// loop state of one registration, so the run can be stepped from the host
+struct RunState {
+    bool active = false, done = false, stage_open = false;
+    nrr_solver_config cfg{};
+    std::vector<int> lm_idx;
+    std::vector<double> lm_pos;
+    Params prm;
+    Window win;
+    int si = 0, accepted = 0, passes = 0, degenerate_total = 0;
+    nrr_stage_record st{};
+    double lm_w = 0.0, e_prev = 0.0;
+    bool current_is_aa = false;
+    std::chrono::steady_clock::time_point t0, t1;
+};
+
+}  // namespace nrr_b200
+
+using namespace nrr_b200;
+
+struct nrr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 0;
+    size_t smem_optin = 0;
+    nrr_solve_options opt{1e-12, 20000, 0};
+    int64_t launches = 0;
+    bool timing = false;
+
+    // ---- target (SpatialIndex)
+    BvhHost bvh;
+    DevBuf<float4> d_pts, d_lo, d_hi;
+    DevBuf<double> d_tgt;
+    BvhView bv{};
+    bool has_target = false;
+
+    // ---- problem
+    bool has_problem = false;
+    int n = 0, N = 0, E = 0, P = 0;
+    double src_avg = 0.0;
+    std::vector<int> h_row_ptr, h_col;
+    std::vector<double> h_src;
+    DevBuf<double> d_src, d_infl_w, d_anchor, d_node_pos, d_pair_c;
+    DevBuf<double4> d_infl_f;
+    DevBuf<int> d_infl_off, d_infl_node, d_pairs, d_pair_rev, d_node_pair_off, d_row_ptr, d_col, d_ub_cptr, d_cv,
+        d_cea, d_ceb, d_ub_kpos, d_ub_kpos_t, d_edges, d_edge_pab, d_edge_pba, d_lm_vertex;
+    DevBuf<double> d_lm_pos;
+    DevProblem dp{};
+
+    // ---- per-iteration state
+    DevBuf<double> x, xmm, xnext, vhat, vhat2, d2, q, wa, wr, R, K, B, Z, term_part, pcg_a, pcg_b;
+    DevBuf<int> nn_idx, deg, row_begin;
+    PcgPlan plan;
+    DevBuf<PcgStatus> d_status;
+    DevBuf<PassRecord> d_rec;
+    Pinned<PassRecord> h_rec;
+    Pinned<PcgStatus> h_status;
+    Pinned<int> h_deg;
+    // Anderson
+    int aa_m = 0;
+    size_t aa_dim = 0;
+    DevBuf<double> aa_df, aa_dg, aa_fprev, aa_gprev, aa_theta, aa_part;
+    DevBuf<int> aa_rank;
+    AADevice aa{};
+
+    // ---- report of the last run
+    nrr_report_summary summary{};
+    std::vector<nrr_stage_record> stages;
+    std::vector<nrr_iteration_record> iters;
+    std::vector<nrr_pass_record> passes;
+    std::vector<int> pass_nn;
+
+    // ---- timing (CUDA events per kernel class)
+    static constexpr int kClasses = 6;
+    cudaEvent_t ev[kClasses][2] = {};
+    double class_ms[kClasses] = {0};
+    int pcg_iters_total = 0;
+    cudaEvent_t pass_ev[2] = {};
+    RunState run;
+    size_t l2_bytes = 0;
+    DevBuf<double> flush;
+
+    ~nrr_ctx() {
+        for (auto& e : ev)
+            for (auto& x : e)
+                if (x) cudaEventDestroy(x);
+        for (auto& x : pass_ev)
+            if (x) cudaEventDestroy(x);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace nrr_b200 {
+namespace {
+
+enum Cls { kNN = 0, kTerms = 1, kAsm = 2, kPcg = 3, kAA = 4, kDeform = 5 };
+
+struct ClassTimer {
+    nrr_ctx* c;
+    int k;
+    ClassTimer(nrr_ctx* ctx, int cls) : c(ctx), k(cls) {
+        if (c->timing) NRR_CUDA_CHECK(cudaEventRecord(c->ev[k][0], c->stream));
+    }
+    ~ClassTimer() {
+        if (c->timing) cudaEventRecord(c->ev[k][1], c->stream);
+    }
+};
+// after a stream sync: accumulate the elapsed time of every class that ran
+void harvest(nrr_ctx* c, const bool ran[nrr_ctx::kClasses]) {
+    if (!c->timing) return;
+    for (int k = 0; k < nrr_ctx::kClasses; ++k) {
+        if (!ran[k]) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->ev[k][0], c->ev[k][1]) == cudaSuccess) c->class_ms[k] += ms;
+    }
+}
+
+void sync(nrr_ctx* c) { NRR_CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
+
+void require_target(nrr_ctx* c) {
+    if (!c->has_target) throw ConfigError("no target uploaded (nrr_ctx_set_target)");
+}
+void require_problem(nrr_ctx* c) {
+    if (!c->has_problem) throw ConfigError("no problem uploaded (nrr_ctx_set_problem)");
+}
+
+void nn_run(nrr_ctx* c, const double* queries, int nq, const int* prev, int* idx, double* d2, double* q,
+            const double* anchor) {
+    ClassTimer t(c, kNN);
+    launch_nn(c->bv, queries, nq, prev, idx, d2, q, anchor, c->stream);
+    ++c->launches;
+}
+
+void set_target(nrr_ctx* c, const double* tgt, int m) {
+    if (m <= 0) throw NumericalError("SpatialIndex: cannot index an empty point set");
+    c->bvh.build(tgt, m);
+    c->d_tgt.upload(tgt, static_cast<size_t>(m) * 3, c->stream);
+    c->d_pts.upload(c->bvh.pts.data(), c->bvh.pts.size(), c->stream);
+    c->d_lo.upload(c->bvh.box_lo.data(), c->bvh.box_lo.size(), c->stream);
+    c->d_hi.upload(c->bvh.box_hi.data(), c->bvh.box_hi.size(), c->stream);
+    BvhView& b = c->bv;
+    b.pts = c->d_pts.p;
+    b.box_lo = c->d_lo.p;
+    b.box_hi = c->d_hi.p;
+    b.tgt64 = c->d_tgt.p;
+    b.m = m;
+    b.levels = static_cast<int>(c->bvh.level_cnt.size());
+    for (int l = 0; l < kMaxLevels; ++l) {
+        b.level_off[l] = l < b.levels ? c->bvh.level_off[l] : 0;
+        b.level_cnt[l] = l < b.levels ? c->bvh.level_cnt[l] : 0;
+    }
+    b.cx = c->bvh.center[0];
+    b.cy = c->bvh.center[1];
+    b.cz = c->bvh.center[2];
+    b.half_extent = static_cast<float>(c->bvh.half_extent);
+    c->has_target = true;
+}
+
+// SystemAssembler ctor (energy.hpp:139-176) + the B200 assembly plan
+void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
+    const int n = p->n, N = p->node_count, E = p->edge_count, P = p->pair_count;
+    if (n < 0 || N < 0 || E < 0 || P < 0) throw ConfigError("negative problem size");
+    if (N == 0 && n > 0) throw ConfigError("deformation graph has no nodes");
+    cudaStream_t s = c->stream;
+    c->n = n;
+    c->N = N;
+    c->E = E;
+    c->P = P;
+    c->src_avg = p->src_avg_edge_length;
+    c->h_src.assign(p->source, p->source + 3 * static_cast<size_t>(n));
+    const int sumk = n > 0 ? p->infl_offsets[n] : 0;
+    // constant per-influence f = w [v - p; 1] and the anchor sum w p (energy.hpp:150-161)
+    std::vector<double4> f(sumk);
+    std::vector<double> anchor(3 * static_cast<size_t>(n), 0.0);
+    for (int i = 0; i < n; ++i) {
+        const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
+        if (k1 <= k0) throw NumericalError("source point without influencing nodes");
+        for (int k = k0; k < k1; ++k) {
+            const int a = p->infl_nodes[k];
+            if (a < 0 || a >= N) throw ConfigError("influence node index out of range");
+            const double w = p->infl_weights[k];
+            const double* pa = p->node_positions + 3 * a;
+            const double* v = p->source + 3 * i;
+            f[k] = make_double4(w * (v[0] - pa[0]), w * (v[1] - pa[1]), w * (v[2] - pa[2]), w);
+            for (int cc = 0; cc < 3; ++cc) anchor[3 * i + cc] += w * pa[cc];
+        }
+    }
+    // BSR pattern: diagonal + both halves of each edge (energy.hpp:264-279)
+    std::vector<std::vector<int>> cols(N);
+    for (int j = 0; j < N; ++j) cols[j].push_back(j);
+    for (int e = 0; e < E; ++e) {
+        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
+        if (a < 0 || b < 0 || a >= N || b >= N || a == b) throw ConfigError("graph edge index out of range");
+        cols[a].push_back(b);
+        cols[b].push_back(a);
+    }
+    c->h_row_ptr.assign(N + 1, 0);
+    c->h_col.clear();
+    for (int j = 0; j < N; ++j) {
+        std::sort(cols[j].begin(), cols[j].end());
+        cols[j].erase(std::unique(cols[j].begin(), cols[j].end()), cols[j].end());
+        c->h_row_ptr[j + 1] = c->h_row_ptr[j] + static_cast<int>(cols[j].size());
+        c->h_col.insert(c->h_col.end(), cols[j].begin(), cols[j].end());
+    }
+    const int nnzb = c->h_row_ptr[N];
+    auto find_blk = [&](int a, int b) -> int {
+        const auto lo = c->h_col.begin() + c->h_row_ptr[a], hi = c->h_col.begin() + c->h_row_ptr[a + 1];
+        const auto it = std::lower_bound(lo, hi, b);
+        if (it == hi || *it != b) return -1;
+        return static_cast<int>(it - c->h_col.begin());
+    };
+    // edge index per (a<b) block for the contributor lists
+    std::vector<int> edge_of_blk(nnzb, -1);
+    for (int e = 0; e < E; ++e) {
+        const int a = std::min(p->edges[2 * e], p->edges[2 * e + 1]);
+        const int b = std::max(p->edges[2 * e], p->edges[2 * e + 1]);
+        edge_of_blk[find_blk(a, b)] = e;
+    }
+    // contributor lists per upper block, in vertex order (the reference's program order)
+    const int U = N + E;
+    std::vector<int> cnt(U + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
+        for (int ka = k0; ka < k1; ++ka) {
+            ++cnt[p->infl_nodes[ka]];
+            for (int kb = k0; kb < k1; ++kb) {
+                const int a = p->infl_nodes[ka], b = p->infl_nodes[kb];
+                if (a >= b) continue;
+                const int blk = find_blk(a, b);
+                if (blk < 0) throw NumericalError("assemble: co-influencing node pair is not a graph edge");
+                ++cnt[N + edge_of_blk[blk]];
+            }
+        }
+    }
+    std::vector<int> cptr(U + 1, 0);
+    for (int u = 0; u < U; ++u) cptr[u + 1] = cptr[u] + cnt[u];
+    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+    std::vector<int> cv(cptr[U]), cea(cptr[U]), ceb(cptr[U]);
+    for (int i = 0; i < n; ++i) {
+        const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
+        for (int ka = k0; ka < k1; ++ka) {
+            const int a = p->infl_nodes[ka];
+            int t = fill[a]++;
+            cv[t] = i;
+            cea[t] = ka;
+            ceb[t] = ka;
+            for (int kb = k0; kb < k1; ++kb) {
+                const int b = p->infl_nodes[kb];
+                if (a >= b) continue;
+                const int u = N + edge_of_blk[find_blk(a, b)];
+                t = fill[u]++;
+                cv[t] = i;
+                cea[t] = ka;
+                ceb[t] = kb;
+            }
+        }
+    }
+    std::vector<int> kpos(U), kpos_t(U), eab(E), eba(E);
+    for (int j = 0; j < N; ++j) kpos[j] = kpos_t[j] = find_blk(j, j);
+    // directed pairs: i-major ranges, reverse index
+    std::vector<int> npo(N + 1, 0);
+    for (int e = 0; e < P; ++e) {
+        const int i = p->reg_pairs[2 * e];
+        if (i < 0 || i >= N) throw ConfigError("reg pair index out of range");
+        if (e > 0 && p->reg_pairs[2 * (e - 1)] > i) throw ConfigError("reg pairs must be i-major");
+        ++npo[i + 1];
+    }
+    for (int j = 0; j < N; ++j) npo[j + 1] += npo[j];
+    std::vector<int> rev(P, -1);
+    auto pair_index = [&](int i, int j) -> int {
+        for (int e = npo[i]; e < npo[i + 1]; ++e)
+            if (p->reg_pairs[2 * e + 1] == j) return e;
+        return -1;
+    };
+    for (int e = 0; e < P; ++e) {
+        rev[e] = pair_index(p->reg_pairs[2 * e + 1], p->reg_pairs[2 * e]);
+        if (rev[e] < 0) throw ConfigError("reg pairs are not symmetric");
+    }
+    for (int e = 0; e < E; ++e) {
+        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
+        kpos[N + e] = find_blk(a, b);
+        kpos_t[N + e] = find_blk(b, a);
+        eab[e] = pair_index(a, b);
+        eba[e] = pair_index(b, a);
+        if ((eab[e] < 0 || eba[e] < 0) && P > 0) throw ConfigError("graph edge without reg pairs");
+    }
+    if (P == 0 && E > 0) throw ConfigError("graph edges without reg pairs");
+    // upload
+    c->d_src.upload(p->source, 3 * static_cast<size_t>(n), s);
+    c->d_infl_off.upload(p->infl_offsets, n + 1, s);
+    c->d_infl_node.upload(p->infl_nodes, sumk, s);
+    c->d_infl_w.upload(p->infl_weights, sumk, s);
+    c->d_infl_f.upload(f.data(), sumk, s);
+    c->d_anchor.upload(anchor.data(), anchor.size(), s);
+    c->d_node_pos.upload(p->node_positions, 3 * static_cast<size_t>(N), s);
+    c->d_pairs.upload(p->reg_pairs, 2 * static_cast<size_t>(P), s);
+    c->d_pair_c.upload(p->reg_weights, P, s);
+    c->d_pair_rev.upload(rev.data(), P, s);
+    c->d_node_pair_off.upload(npo.data(), N + 1, s);
+    c->d_row_ptr.upload(c->h_row_ptr.data(), N + 1, s);
+    c->d_col.upload(c->h_col.data(), nnzb, s);
+    c->d_ub_cptr.upload(cptr.data(), U + 1, s);
+    c->d_cv.upload(cv.data(), cv.size(), s);
+    c->d_cea.upload(cea.data(), cea.size(), s);
+    c->d_ceb.upload(ceb.data(), ceb.size(), s);
+    c->d_ub_kpos.upload(kpos.data(), U, s);
+    c->d_ub_kpos_t.upload(kpos_t.data(), U, s);
+    c->d_edges.upload(p->edges, 2 * static_cast<size_t>(E), s);
+    c->d_edge_pab.upload(eab.data(), E, s);
+    c->d_edge_pba.upload(eba.data(), E, s);
+    DevProblem& d = c->dp;
+    d = DevProblem{};
+    d.n = n;
+    d.N = N;
+    d.E = E;
+    d.P = P;
+    d.U = U;
+    d.nnzb = nnzb;
+    d.src = c->d_src.p;
+    d.infl_off = c->d_infl_off.p;
+    d.infl_node = c->d_infl_node.p;
+    d.infl_w = c->d_infl_w.p;
+    d.infl_f = c->d_infl_f.p;
+    d.anchor = c->d_anchor.p;
+    d.node_pos = c->d_node_pos.p;
+    d.pairs = c->d_pairs.p;
+    d.pair_c = c->d_pair_c.p;
+    d.pair_rev = c->d_pair_rev.p;
+    d.node_pair_off = c->d_node_pair_off.p;
+    d.row_ptr = c->d_row_ptr.p;
+    d.col = c->d_col.p;
+    d.ub_cptr = c->d_ub_cptr.p;
+    d.c_v = c->d_cv.p;
+    d.c_ea = c->d_cea.p;
+    d.c_eb = c->d_ceb.p;
+    d.ub_kpos = c->d_ub_kpos.p;
+    d.ub_kpos_t = c->d_ub_kpos_t.p;
+    d.edges = c->d_edges.p;
+    d.edge_pab = c->d_edge_pab.p;
+    d.edge_pba = c->d_edge_pba.p;
+    // state buffers
+    const size_t D = 12 * static_cast<size_t>(N);
+    for (auto* b : {&c->x, &c->xmm, &c->xnext, &c->B, &c->Z}) b->resize(std::max<size_t>(D, 1));
+    for (auto* b : {&c->vhat, &c->vhat2, &c->q}) b->resize(std::max<size_t>(3 * static_cast<size_t>(n), 1));
+    c->d2.resize(std::max(n, 1));
+    c->wa.resize(std::max(n, 1));
+    c->nn_idx.resize(std::max(n, 1));
+    c->wr.resize(std::max(P, 1));
+    c->R.resize(std::max<size_t>(9 * static_cast<size_t>(N), 1));
+    c->K.resize(std::max<size_t>(16 * static_cast<size_t>(nnzb), 1));
+    c->term_part.resize(3 * kTermBlocks);
+    c->deg.resize(1);
+    c->d_rec.resize(1);
+    c->d_status.resize(1);
+    if (N > 0) {
+        c->plan.build(c->h_row_ptr.data(), N, c->num_sms, c->smem_optin);
+        c->row_begin.upload(c->plan.row_begin.data(), c->plan.row_begin.size(), s);
+        c->pcg_a.resize(8 * static_cast<size_t>(c->plan.grid));
+        c->pcg_b.resize(8 * static_cast<size_t>(c->plan.grid));
+    }
+    NRR_CUDA_CHECK(cudaStreamSynchronize(s));
+    c->has_problem = true;
+}
+
+void ensure_aa(nrr_ctx* c, int m, size_t D) {
+    if (m > kMaxAA) throw ConfigError("aa_window above the device limit of 16");
+    const int mm = std::max(m, 1);
+    if (c->aa_m != mm || c->aa_dim != D) {
+        c->aa_df.resize(mm * D);
+        c->aa_dg.resize(mm * D);
+        c->aa_fprev.resize(D);
+        c->aa_gprev.resize(D);
+        c->aa_theta.resize(kMaxAA);
+        c->aa_part.resize(static_cast<size_t>(kTriMax) * kTermBlocks);
+        c->aa_rank.resize(1);
+        c->aa_m = mm;
+        c->aa_dim = D;
+    }
+    c->aa.df = c->aa_df.p;
+    c->aa.dg = c->aa_dg.p;
+    c->aa.fprev = c->aa_fprev.p;
+    c->aa.gprev = c->aa_gprev.p;
+    c->aa.theta = c->aa_theta.p;
+    c->aa.partials = c->aa_part.p;
+    c->aa.rank = c->aa_rank.p;
+}
+
+SlotList to_slots(const std::vector<int>& v) {
+    SlotList s{};
+    s.n = static_cast<int>(v.size());
+    for (int k = 0; k < s.n; ++k) s.s[k] = v[k];
+    return s;
+}
+
+// push (g, f = g - x) and combine into x_next (anderson.hpp:22-46)
+void aa_push_combine(nrr_ctx* c, Window& w, const double* g, const double* x, const double* f, double* x_next,
+                     int D) {
+    ClassTimer t(c, kAA);
+    const int have_prev = w.hist >= 1 && w.m > 0;
+    int slot = -1;
+    if (have_prev) {
+        slot = (w.newest + 1) % w.m;
+        w.newest = slot;
+        w.cols.insert(w.cols.begin(), slot);
+        if (static_cast<int>(w.cols.size()) > w.m) w.cols.pop_back();
+    }
+    w.hist = std::min(w.hist + 1, w.m + 1);
+    const SlotList cols = to_slots(w.cols);
+    launch_aa_update(c->aa, g, x, f, D, have_prev, slot < 0 ? 0 : slot, c->stream);
+    ++c->launches;
+    const int mk = std::min(w.hist - 1, w.m);
+    if (mk <= 0) {
+        NRR_CUDA_CHECK(cudaMemcpyAsync(x_next, g, sizeof(double) * D, cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    launch_aa_solve(c->aa, D, cols, c->stream);
+    launch_aa_combine(c->aa, D, cols, x_next, &c->d_rec.p->nonfinite, c->stream);
+    c->launches += 3;
+}
+
+void validate(const nrr_solver_config& cfg) {  // solver.hpp:32-38
+    if (!(cfg.eps > 0.0)) throw ConfigError("eps must be positive");
+    if (cfg.i_max < 1) throw ConfigError("i_max must be at least 1");
+    if (cfg.aa_window < 0) throw ConfigError("aa_window must be >= 0");
+    if (cfg.k_alpha < 0.0 || cfg.k_beta < 0.0) throw ConfigError("k_alpha and k_beta must be non-negative");
+}
+
+void update_term_weights(Params& p, int n, int E, int N, const nrr_solver_config& cfg) {  // solver.hpp:68-80
+    if (E == 0) {
+        p.alpha = 0.0;
+        p.forced_zero = true;
+    } else {
+        p.alpha = cfg.k_alpha * (static_cast<double>(n) / E) * (p.nu_r * p.nu_r) / (p.nu_a * p.nu_a);
+    }
+    p.beta = cfg.k_beta * (static_cast<double>(n) / N) / (2.0 * p.nu_a * p.nu_a);
+}
+
+Params init_parameters(nrr_ctx* c, const nrr_solver_config& cfg) {  // solver.hpp:86-106
+    require_target(c);
+    require_problem(c);
+    const int n = c->n;
+    nn_run(c, c->d_src.p, n, nullptr, c->nn_idx.p, c->d2.p, nullptr, nullptr);
+    std::vector<double> dist(n);
+    NRR_CUDA_CHECK(cudaMemcpyAsync(dist.data(), c->d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    for (auto& d : dist) d = std::sqrt(d);
+    double median = 0.0;
+    if (n > 0) {
+        std::sort(dist.begin(), dist.end());
+        median = n % 2 == 1 ? dist[n / 2] : 0.5 * (dist[n / 2 - 1] + dist[n / 2]);
+    }
+    Params p;
+    const double l_bar = c->src_avg;
+    p.nu_a_min = std::isnan(cfg.nu_a_min) ? l_bar / std::sqrt(3.0) : cfg.nu_a_min;
+    p.nu_a = std::isnan(cfg.nu_a_init) ? std::max(median, p.nu_a_min) : cfg.nu_a_init;
+    p.nu_r = std::isnan(cfg.nu_r_init) ? 3.0 * l_bar : cfg.nu_r_init;
+    if (!(p.nu_a > 0.0) || !(p.nu_r > 0.0)) throw NumericalError("init_parameters: Welsch parameters must be positive");
+    update_term_weights(p, n, c->E, c->N, cfg);
+    return p;
+}
+
+void upload_landmarks(nrr_ctx* c, const nrr_solver_config& cfg) {
+    const int L = cfg.landmark_count;
+    for (int l = 0; l < L; ++l)
+        if (cfg.landmark_index[l] < 0 || cfg.landmark_index[l] >= c->n)
+            throw ConfigError("landmark source index out of range");
+    c->dp.landmarks = L;
+    if (L > 0) {
+        c->d_lm_vertex.upload(cfg.landmark_index, L, c->stream);
+        c->d_lm_pos.upload(cfg.landmark_pos, 3 * static_cast<size_t>(L), c->stream);
+        c->dp.lm_vertex = c->d_lm_vertex.p;
+        c->dp.lm_pos = c->d_lm_pos.p;
+    }
+}
+
+void set_identity(nrr_ctx* c, double* x) {
+    std::vector<double> h(12 * static_cast<size_t>(c->N), 0.0);
+    for (int j = 0; j < c->N; ++j)
+        for (int r = 0; r < 3; ++r) h[12 * j + 3 * r + r] = 1.0;
+    NRR_CUDA_CHECK(cudaMemcpyAsync(x, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, c->stream));
+    sync(c);  // h is stack memory
+}
+
+void deform_run(nrr_ctx* c, const double* x, double* out, const double* old, double* max_disp) {
+    ClassTimer t(c, kDeform);
+    launch_deform(c->dp, x, out, old, max_disp, &c->d_rec.p->nonfinite, c->stream);
+    ++c->launches;
+}
+
+// evaluate the pass at (x, vhat): correspondences, weights, energies
+void evaluate(nrr_ctx* c, const double* x, const double* vhat, const TermParams& tp, bool warm) {
+    nn_run(c, vhat, c->n, warm ? c->nn_idx.p : nullptr, c->nn_idx.p, c->d2.p, c->q.p, c->d_anchor.p);
+    ClassTimer t(c, kTerms);
+    NRR_CUDA_CHECK(cudaMemsetAsync(c->deg.p, 0, sizeof(int), c->stream));
+    launch_terms(c->dp, x, c->d2.p, tp, c->wa.p, c->wr.p, c->R.p, c->term_part.p, c->deg.p, c->stream);
+    launch_energy_reduce(c->dp, c->term_part.p, tp, vhat, c->d_rec.p, c->stream);
+    c->launches += 2;
+}
+
+void assemble_solve(nrr_ctx* c, const TermParams& tp, const double* x0, double* xout) {
+    {
+        ClassTimer t(c, kAsm);
+        launch_assemble(c->dp, c->wa.p, c->q.p, c->wr.p, c->R.p, tp, c->K.p, c->B.p, c->stream);
+        c->launches += (tp.lm_weight != 0.0 && c->dp.landmarks > 0) ? 2 : 1;
+    }
+    ClassTimer t(c, kPcg);
+    if (xout != x0)
+        NRR_CUDA_CHECK(cudaMemcpyAsync(xout, x0, sizeof(double) * 12 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+    PcgStatus init{0x7fffffff, 0, 0, 0, 0.0};
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->d_status.p, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    PcgArgs a{};
+    a.row_ptr = c->d_row_ptr.p;
+    a.col = c->d_col.p;
+    a.K = c->K.p;
+    a.B = c->B.p;
+    a.X = xout;
+    a.Z = c->Z.p;
+    a.row_begin = c->row_begin.p;
+    a.part_a = c->pcg_a.p;
+    a.part_b = c->pcg_b.p;
+    a.status = c->d_status.p;
+    a.rtol = c->opt.pcg_rtol;
+    a.max_iter = c->opt.pcg_max_iter;
+    launch_pcg(c->plan, a, c->stream);
+    ++c->launches;
+}
+
+void check_pcg(nrr_ctx* c, const PcgStatus& st) {
+    if (st.fail_node != 0x7fffffff)
+        throw NumericalError("linear system not positive definite (singular diagonal block at node " +
+                             std::to_string(st.fail_node) + ")");
+    if (st.code == 2)
+        throw NumericalError("linear system not positive definite (indefinite coupling between node blocks)");
+    if (st.code != 1) throw NumericalError("linear solve residual above tolerance");
+}
+
+// ---- resumable register_surfaces state machine (solver.hpp:180-304) ----
+void run_begin(nrr_ctx* c, const nrr_solver_config& cfg_in) {
+    validate(cfg_in);
+    require_target(c);
+    require_problem(c);
+    if (c->n == 0 || c->bv.m == 0) throw NumericalError("register_surfaces: empty surface");
+    RunState& r = c->run;
+    r = RunState{};
+    r.t0 = std::chrono::steady_clock::now();
+    r.cfg = cfg_in;
+    r.lm_idx.assign(cfg_in.landmark_index, cfg_in.landmark_index + cfg_in.landmark_count);
+    r.lm_pos.assign(cfg_in.landmark_pos, cfg_in.landmark_pos + 3 * cfg_in.landmark_count);
+    r.cfg.landmark_index = r.lm_idx.data();
+    r.cfg.landmark_pos = r.lm_pos.data();
+    for (double& v : c->class_ms) v = 0.0;
+    c->pcg_iters_total = 0;
+    c->stages.clear();
+    c->iters.clear();
+    c->passes.clear();
+    c->pass_nn.clear();
+    upload_landmarks(c, r.cfg);
+    r.prm = init_parameters(c, r.cfg);
+    ensure_aa(c, r.cfg.aa_window, 12 * c->N);
+    r.win.m = r.cfg.aa_window;
+    set_identity(c, c->x.p);
+    NRR_CUDA_CHECK(cudaMemsetAsync(c->d_rec.p, 0, sizeof(PassRecord), c->stream));
+    deform_run(c, c->x.p, c->vhat.p, nullptr, nullptr);
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->xmm.p, c->x.p, sizeof(double) * 12 * c->N, cudaMemcpyDeviceToDevice, c->stream));
+    sync(c);
+    r.t1 = std::chrono::steady_clock::now();
+    r.active = true;
+}
+
+void open_stage(nrr_ctx* c) {
+    RunState& r = c->run;
+    r.st = nrr_stage_record{r.prm.nu_a, r.prm.nu_r, r.prm.alpha, r.prm.beta, 0, 0,
+                            static_cast<int32_t>(c->iters.size()), 0};
+    r.lm_w = (r.si == 0 && r.cfg.landmark_count > 0) ? 1.0 : 0.0;
+    r.win.reset();
+    r.e_prev = std::numeric_limits<double>::infinity();
+    r.accepted = 0;
+    r.passes = 0;
+    r.stage_open = true;
+}
+
+void close_stage(nrr_ctx* c) {
+    RunState& r = c->run;
+    c->stages.push_back(r.st);
+    r.stage_open = false;
+    ++r.si;
+    if (r.prm.nu_a == r.prm.nu_a_min) {  // anneal (solver.hpp:60-64, 292-293)
+        r.done = true;
+        return;
+    }
+    r.prm.nu_a = std::max(r.prm.nu_a / 2.0, r.prm.nu_a_min);
+    r.prm.nu_r = std::max(r.prm.nu_r / 2.0, r.cfg.nu_r_floor);
+    update_term_weights(r.prm, c->n, c->E, c->N, r.cfg);
+}
+
+// One evaluated pass (solver.hpp:225-288). Returns true when an iteration was
+// accepted; sets *stage_end when the stage converged or hit i_max.
+bool one_pass(nrr_ctx* c, bool* stage_end) {
+    RunState& r = c->run;
+    const int N = c->N, n = c->n, D = 12 * N;
+    *stage_end = false;
+    if (++r.passes > 2 * r.cfg.i_max + 4) throw NumericalError("solver stage failed to make progress");
+    const TermParams tp{r.prm.alpha, r.prm.beta, r.prm.nu_a, r.prm.nu_r, r.lm_w};
+    bool ran[nrr_ctx::kClasses];
+    std::fill(ran, ran + nrr_ctx::kClasses, false);
+    NRR_CUDA_CHECK(cudaMemsetAsync(c->d_rec.p, 0, sizeof(PassRecord), c->stream));
+    // warm start from the previous pass's correspondences (init NN at the first pass)
+    evaluate(c, c->x.p, c->vhat.p, tp, true);
+    ran[kNN] = ran[kTerms] = true;
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_deg.p, c->deg.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (c->opt.record_passes == 2) {
+        c->pass_nn.resize(c->pass_nn.size() + n);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(c->pass_nn.data() + c->pass_nn.size() - n, c->nn_idx.p, sizeof(int) * n,
+                                       cudaMemcpyDeviceToHost, c->stream));
+    }
+    sync(c);
+    harvest(c, ran);
+    const PassRecord e = *c->h_rec.p;
+    r.degenerate_total += *c->h_deg.p;
+    const double e_accept = e.total + r.lm_w * e.landmark;
+    if (!std::isfinite(e_accept)) throw NumericalError("solver aborted: energy is not finite");
+    const bool revert = e_accept > r.e_prev && r.current_is_aa;  // solver.hpp:239
+    if (c->opt.record_passes) c->passes.push_back({e.total, r.si, revert ? 1 : 0});
+    if (revert) {  // solver.hpp:244-248
+        NRR_CUDA_CHECK(cudaMemcpyAsync(c->x.p, c->xmm.p, sizeof(double) * D, cudaMemcpyDeviceToDevice, c->stream));
+        deform_run(c, c->x.p, c->vhat.p, nullptr, nullptr);
+        r.current_is_aa = false;
+        ++r.st.reverts;
+        return false;
+    }
+    r.e_prev = e_accept;
+    nrr_iteration_record rec{e.total, e.align, e.reg, e.rot, e.landmark, 0.0, r.current_is_aa ? 1 : 0, r.si};
+    std::fill(ran, ran + nrr_ctx::kClasses, false);
+    assemble_solve(c, tp, c->x.p, c->xmm.p);  // x_mm = solve(), warm start at x
+    ran[kAsm] = ran[kPcg] = true;
+    aa_push_combine(c, r.win, c->xmm.p, c->x.p, nullptr, c->xnext.p, D);
+    ran[kAA] = true;
+    r.current_is_aa = r.win.extrapolating();
+    NRR_CUDA_CHECK(cudaMemsetAsync(&c->d_rec.p->max_disp, 0, sizeof(double), c->stream));
+    deform_run(c, c->xnext.p, c->vhat2.p, c->vhat.p, &c->d_rec.p->max_disp);
+    ran[kDeform] = true;
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_status.p, c->d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    harvest(c, ran);
+    check_pcg(c, *c->h_status.p);
+    c->pcg_iters_total += c->h_status.p->iterations;
+    if (c->h_rec.p->nonfinite) throw NumericalError("solver aborted: iterate is not finite");
+    rec.max_disp = c->h_rec.p->max_disp;
+    c->iters.push_back(rec);
+    ++r.st.iteration_count;
+    std::swap(c->x.p, c->xnext.p);
+    std::swap(c->vhat.p, c->vhat2.p);
+    ++r.accepted;
+    if (rec.max_disp < r.cfg.eps) {
+        r.st.converged = 1;
+        *stage_end = true;
+    } else if (r.accepted >= r.cfg.i_max) {
+        *stage_end = true;
+    }
+    return true;
+}
+
+// Runs passes until `max_accepted` more iterations were accepted or the run
+// finished. Device time of the passes (CUDA events on the context stream,
+// excluding the optional L2 flush before each pass) is added to *device_ms.
+int run_iterate(nrr_ctx* c, int max_accepted, bool flush_l2, double* device_ms) {
+    RunState& r = c->run;
+    if (!r.active) throw ConfigError("no registration in progress (nrr_ctx_begin)");
+    int acc = 0;
+    if (flush_l2 && c->flush.n == 0) c->flush.resize(c->l2_bytes * 2 / sizeof(double) + 1);
+    while (!r.done && acc < max_accepted) {
+        if (!r.stage_open) open_stage(c);
+        if (flush_l2) NRR_CUDA_CHECK(cudaMemsetAsync(c->flush.p, acc & 0xff, c->flush.n * sizeof(double), c->stream));
+        NRR_CUDA_CHECK(cudaEventRecord(c->pass_ev[0], c->stream));
+        bool stage_end = false;
+        const bool accepted = one_pass(c, &stage_end);
+        NRR_CUDA_CHECK(cudaEventRecord(c->pass_ev[1], c->stream));
+        NRR_CUDA_CHECK(cudaEventSynchronize(c->pass_ev[1]));
+        float ms = 0.f;
+        NRR_CUDA_CHECK(cudaEventElapsedTime(&ms, c->pass_ev[0], c->pass_ev[1]));
+        if (device_ms) *device_ms += ms;
+        if (accepted) ++acc;
+        if (stage_end) close_stage(c);
+    }
+    return acc;
+}
+
+void run_finish(nrr_ctx* c, double* out_X, double* out_deformed) {
+    RunState& r = c->run;
+    if (!r.active) throw ConfigError("no registration in progress (nrr_ctx_begin)");
+    if (r.stage_open) close_stage(c);  // stopped early: record the partial stage
+    const auto t2 = std::chrono::steady_clock::now();
+    const int N = c->N, n = c->n;
+    if (out_X) {
+        launch_nodemajor_to_colmajor(c->x.p, c->xnext.p, N, c->stream);
+        ++c->launches;
+        NRR_CUDA_CHECK(cudaMemcpyAsync(out_X, c->xnext.p, sizeof(double) * 12 * N, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (out_deformed)
+        NRR_CUDA_CHECK(cudaMemcpyAsync(out_deformed, c->vhat.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    nrr_report_summary& s = c->summary;
+    s.stage_count = static_cast<int32_t>(c->stages.size());
+    s.total_iterations = static_cast<int32_t>(c->iters.size());
+    s.degenerate_rotations = r.degenerate_total;
+    s.alpha_forced_zero = r.prm.forced_zero ? 1 : 0;
+    s.total_passes = 0;
+    for (const auto& stg : c->stages) s.total_passes += stg.iteration_count + stg.reverts;
+    s.linear_iterations = c->pcg_iters_total;
+    s.setup_seconds = std::chrono::duration<double>(r.t1 - r.t0).count();
+    s.loop_seconds = std::chrono::duration<double>(t2 - r.t1).count();
+    s.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - r.t0).count();
+    r.active = false;
+}
+
+void run_register(nrr_ctx* c, const nrr_solver_config& cfg, double* out_X, double* out_deformed) {
+    run_begin(c, cfg);
+    run_iterate(c, std::numeric_limits<int>::max(), false, nullptr);
+    run_finish(c, out_X, out_deformed);
+}
+
+}  // namespace
+}  // namespace nrr_b200
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* nrr_last_error(void) { return nrr_b200::g_last_error.c_str(); }
+
+int nrr_device_info(int device, char* name, int32_t cap, int32_t* sm_count) {
+    return guarded([&] {
+        cudaDeviceProp prop{};
+        NRR_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        if (name && cap > 0) {
+            std::strncpy(name, prop.name, cap - 1);
+            name[cap - 1] = 0;
+        }
+        if (sm_count) *sm_count = prop.multiProcessorCount;
+    });
+}
+
+int nrr_ctx_create(int device, nrr_ctx** out) {
+    return guarded([&] {
+        *out = nullptr;
+        int count = 0;
+        NRR_CUDA_CHECK(cudaGetDeviceCount(&count));
+        if (count == 0) throw CudaError("no CUDA device");
+        NRR_CUDA_CHECK(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        NRR_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) throw CudaError("nrr_b200 needs an sm_100a device (B200)");
+        auto c = std::make_unique<nrr_ctx>();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        c->smem_optin = prop.sharedMemPerBlockOptin;
+        NRR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->d_rec.resize(1);
+        c->d_status.resize(1);
+        c->deg.resize(1);
+        for (auto& e : c->ev)
+            for (auto& x : e) NRR_CUDA_CHECK(cudaEventCreate(&x));
+        for (auto& x : c->pass_ev) NRR_CUDA_CHECK(cudaEventCreate(&x));
+        c->l2_bytes = prop.l2CacheSize;
+        *out = c.release();
+    });
+}
+
+void nrr_ctx_destroy(nrr_ctx* ctx) { delete ctx; }
+
+int nrr_ctx_set_options(nrr_ctx* ctx, const nrr_solve_options* opt) {
+    return guarded([&] {
+        if (!(opt->pcg_rtol > 0.0) || opt->pcg_max_iter < 1) throw ConfigError("invalid solve options");
+        ctx->opt = *opt;
+    });
+}
+
+int nrr_ctx_enable_timing(nrr_ctx* ctx, int32_t on) {
+    ctx->timing = on != 0;
+    return 0;
+}
+
+int nrr_ctx_set_target(nrr_ctx* ctx, const double* target, int32_t m) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        set_target(ctx, target, m);
+        NRR_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int nrr_ctx_set_problem(nrr_ctx* ctx, const nrr_problem_view* p) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (p->m > 0 && p->target) set_target(ctx, p->target, p->m);
+        set_problem(ctx, p);
+    });
+}
+
+int nrr_ctx_register(nrr_ctx* ctx, const nrr_solver_config* cfg, double* out_X, double* out_deformed) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        run_register(ctx, *cfg, out_X, out_deformed);
+    });
+}
+
+int nrr_ctx_begin(nrr_ctx* ctx, const nrr_solver_config* cfg) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        run_begin(ctx, *cfg);
+    });
+}
+
+int nrr_ctx_iterate(nrr_ctx* ctx, int32_t max_accepted, int32_t flush_l2, int32_t* accepted, int32_t* done,
+                    double* device_ms) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        double ms = 0.0;
+        const int acc = run_iterate(ctx, max_accepted, flush_l2 != 0, &ms);
+        if (accepted) *accepted = acc;
+        if (done) *done = ctx->run.done ? 1 : 0;
+        if (device_ms) *device_ms = ms;
+    });
+}
+
+int nrr_ctx_finish(nrr_ctx* ctx, double* out_X, double* out_deformed) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        run_finish(ctx, out_X, out_deformed);
+    });
+}
+
+int nrr_register(nrr_ctx* ctx, const nrr_problem_view* p, const nrr_solver_config* cfg, double* out_X,
+                 double* out_deformed) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        validate(*cfg);
+        if (p->n == 0 || p->m == 0) throw NumericalError("register_surfaces: empty surface");
+        set_target(ctx, p->target, p->m);
+        set_problem(ctx, p);
+        run_register(ctx, *cfg, out_X, out_deformed);
+    });
+}
+
+int nrr_ctx_report(nrr_ctx* ctx, nrr_report_summary* summary, nrr_stage_record* stages, int32_t stage_cap,
+                   nrr_iteration_record* iters, int32_t iter_cap, nrr_pass_record* passes, int32_t pass_cap,
+                   int32_t* pass_nn_index) {
+    return guarded([&] {
+        if (summary) *summary = ctx->summary;
+        for (int k = 0; stages && k < stage_cap && k < static_cast<int>(ctx->stages.size()); ++k) stages[k] = ctx->stages[k];
+        for (int k = 0; iters && k < iter_cap && k < static_cast<int>(ctx->iters.size()); ++k) iters[k] = ctx->iters[k];
+        const int np = static_cast<int>(ctx->passes.size());
+        for (int k = 0; passes && k < pass_cap && k < np; ++k) passes[k] = ctx->passes[k];
+        if (pass_nn_index && !ctx->pass_nn.empty()) {
+            const size_t cnt = std::min<size_t>(ctx->pass_nn.size(), static_cast<size_t>(pass_cap) * ctx->n);
+            std::memcpy(pass_nn_index, ctx->pass_nn.data(), cnt * sizeof(int));
+        }
+    });
+}
+
+int nrr_nearest(nrr_ctx* ctx, const double* queries, int32_t q, int32_t* out_index, double* out_distance) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        require_target(ctx);
+        if (q <= 0) return;
+        DevBuf<double> dq, dd;
+        DevBuf<int> di;
+        dq.upload(queries, 3 * static_cast<size_t>(q), ctx->stream);
+        dd.resize(q);
+        di.resize(q);
+        nn_run(ctx, dq.p, q, nullptr, di.p, dd.p, nullptr, nullptr);
+        std::vector<double> d2(q);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(out_index, di.p, sizeof(int) * q, cudaMemcpyDeviceToHost, ctx->stream));
+        NRR_CUDA_CHECK(cudaMemcpyAsync(d2.data(), dd.p, sizeof(double) * q, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        for (int i = 0; i < q; ++i) out_distance[i] = std::sqrt(d2[i]);  // kd_tree.hpp:128
+    });
+}
+
+int nrr_deform(nrr_ctx* ctx, const double* X, double* out_points) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        require_problem(ctx);
+        const int N = ctx->N;
+        DevBuf<double> dx;
+        dx.upload(X, 12 * static_cast<size_t>(N), ctx->stream);
+        launch_colmajor_to_nodemajor(dx.p, ctx->xnext.p, N, ctx->stream);
+        NRR_CUDA_CHECK(cudaMemsetAsync(ctx->d_rec.p, 0, sizeof(PassRecord), ctx->stream));
+        deform_run(ctx, ctx->xnext.p, ctx->vhat2.p, nullptr, nullptr);
+        ++ctx->launches;
+        NRR_CUDA_CHECK(cudaMemcpyAsync(out_points, ctx->vhat2.p, sizeof(double) * 3 * ctx->n, cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+        sync(ctx);
+    });
+}
+
+int nrr_project_rotations(nrr_ctx* ctx, const double* X, int32_t N, double* out_R, int32_t* out_degenerate) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        for (int64_t k = 0; k < 12 * static_cast<int64_t>(N); ++k)
+            if (!std::isfinite(X[k])) throw NumericalError("project_to_rotation: non-finite input matrix");
+        DevBuf<double> dx, dn, dr;
+        DevBuf<int> dd;
+        dx.upload(X, 12 * static_cast<size_t>(N), ctx->stream);
+        dn.resize(std::max(12 * N, 1));
+        dr.resize(std::max(9 * N, 1));
+        dd.resize(1);
+        dd.zero(ctx->stream);
+        launch_colmajor_to_nodemajor(dx.p, dn.p, N, ctx->stream);
+        launch_rotations(dn.p, N, dr.p, dd.p, ctx->stream);
+        ctx->launches += 2;
+        NRR_CUDA_CHECK(cudaMemcpyAsync(out_R, dr.p, sizeof(double) * 9 * N, cudaMemcpyDeviceToHost, ctx->stream));
+        int deg = 0;
+        NRR_CUDA_CHECK(cudaMemcpyAsync(&deg, dd.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        if (out_degenerate) *out_degenerate = deg;
+    });
+}
+
+int nrr_step(nrr_ctx* ctx, const double* X, const double* prm, double landmark_weight,
+             const nrr_solver_config* cfg_for_landmarks, int32_t* out_index, double* out_sqdist, double* out_energy4,
+             double* out_K, double* out_B, double* out_Xmm) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        require_target(ctx);
+        require_problem(ctx);
+        const int N = ctx->N, n = ctx->n;
+        if (cfg_for_landmarks) upload_landmarks(ctx, *cfg_for_landmarks);
+        else ctx->dp.landmarks = 0;
+        DevBuf<double> dx;
+        dx.upload(X, 12 * static_cast<size_t>(N), ctx->stream);
+        launch_colmajor_to_nodemajor(dx.p, ctx->x.p, N, ctx->stream);
+        ++ctx->launches;
+        NRR_CUDA_CHECK(cudaMemsetAsync(ctx->d_rec.p, 0, sizeof(PassRecord), ctx->stream));
+        deform_run(ctx, ctx->x.p, ctx->vhat.p, nullptr, nullptr);
+        const TermParams tp{prm[0], prm[1], prm[2], prm[3], landmark_weight};
+        evaluate(ctx, ctx->x.p, ctx->vhat.p, tp, false);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->h_rec.p, ctx->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, ctx->stream));
+        if (out_index)
+            NRR_CUDA_CHECK(cudaMemcpyAsync(out_index, ctx->nn_idx.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        std::vector<double> d2(n);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(d2.data(), ctx->d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        if (out_sqdist)
+            for (int i = 0; i < n; ++i) {
+                const double d = std::sqrt(d2[i]);
+                out_sqdist[i] = d * d;  // corr.squared_distance (energy.hpp:39)
+            }
+        if (out_energy4) {
+            out_energy4[0] = ctx->h_rec.p->align;
+            out_energy4[1] = ctx->h_rec.p->reg;
+            out_energy4[2] = ctx->h_rec.p->rot;
+            out_energy4[3] = ctx->h_rec.p->total;
+        }
+        assemble_solve(ctx, tp, ctx->x.p, ctx->xmm.p);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->h_status.p, ctx->d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+        if (out_K)
+            NRR_CUDA_CHECK(cudaMemcpyAsync(out_K, ctx->K.p, sizeof(double) * 16 * ctx->dp.nnzb, cudaMemcpyDeviceToHost,
+                                           ctx->stream));
+        if (out_B) {
+            launch_nodemajor_to_colmajor(ctx->B.p, ctx->xnext.p, N, ctx->stream);
+            NRR_CUDA_CHECK(cudaMemcpyAsync(out_B, ctx->xnext.p, sizeof(double) * 12 * N, cudaMemcpyDeviceToHost, ctx->stream));
+            sync(ctx);
+        }
+        sync(ctx);
+        if (out_Xmm) {
+            check_pcg(ctx, *ctx->h_status.p);
+            launch_nodemajor_to_colmajor(ctx->xmm.p, ctx->xnext.p, N, ctx->stream);
+            NRR_CUDA_CHECK(cudaMemcpyAsync(out_Xmm, ctx->xnext.p, sizeof(double) * 12 * N, cudaMemcpyDeviceToHost,
+                                           ctx->stream));
+            sync(ctx);
+        }
+    });
+}
+
+int nrr_anderson_combine(nrr_ctx* ctx, const double* G, const double* F, int32_t h, int32_t dim, int32_t m,
+                         double* out, int32_t* out_rank) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (h <= 0) throw NumericalError("anderson_combine: empty history");
+        if (m < 0) throw ConfigError("AndersonWindow: window must be >= 0");
+        const int mk = std::min(h - 1, m);
+        if (mk <= 0) {  // plain update (anderson.hpp:29)
+            std::memcpy(out, G + static_cast<size_t>(h - 1) * dim, sizeof(double) * dim);
+            if (out_rank) *out_rank = 0;
+            return;
+        }
+        ensure_aa(ctx, mk, dim);
+        Window w;
+        w.m = mk;
+        w.reset();
+        DevBuf<double> dg, df, dn;
+        dn.resize(dim);
+        NRR_CUDA_CHECK(cudaMemsetAsync(ctx->d_rec.p, 0, sizeof(PassRecord), ctx->stream));
+        for (int k = h - mk - 1; k < h; ++k) {  // the newest mk+1 entries decide the result
+            dg.upload(G + static_cast<size_t>(k) * dim, dim, ctx->stream);
+            df.upload(F + static_cast<size_t>(k) * dim, dim, ctx->stream);
+            aa_push_combine(ctx, w, dg.p, nullptr, df.p, dn.p, dim);
+            sync(ctx);
+        }
+        int rank = 0;
+        NRR_CUDA_CHECK(cudaMemcpyAsync(out, dn.p, sizeof(double) * dim, cudaMemcpyDeviceToHost, ctx->stream));
+        NRR_CUDA_CHECK(cudaMemcpyAsync(&rank, ctx->aa.rank, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        if (out_rank) *out_rank = rank;
+    });
+}
+
+int nrr_init_parameters(nrr_ctx* ctx, const nrr_solver_config* cfg, double* out6) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        const Params p = init_parameters(ctx, *cfg);
+        out6[0] = p.nu_a;
+        out6[1] = p.nu_r;
+        out6[2] = p.nu_a_min;
+        out6[3] = p.alpha;
+        out6[4] = p.beta;
+        out6[5] = p.forced_zero ? 1.0 : 0.0;
+    });
+}
+
+int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* pcg_iters) {
+    if (launches) *launches = ctx->launches;
+    if (kernel_ms6)
+        for (int k = 0; k < nrr_ctx::kClasses; ++k) kernel_ms6[k] = ctx->class_ms[k];
+    if (pcg_iters) *pcg_iters = ctx->pcg_iters_total;
+    return 0;
+}
+
+}  // extern "C"
