@@ -187,6 +187,11 @@ int nrr_init_parameters(nrr_ctx* ctx, const nrr_solver_config* cfg, double* out6
 int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* pcg_iters);
 int nrr_ctx_enable_timing(nrr_ctx* ctx, int32_t on);
 
+/* host-only probe of the cluster-resident PCG plan for a problem (no device
+ * calls): out8 = {ok, cluster size, max rows per CTA, max smem K blocks,
+ * max ext rows, smem bytes, smem K blocks total, row entries read from L2} */
+int nrr_debug_solver_plan(const nrr_problem_view* p, int32_t num_sms, int64_t smem_limit, int64_t* out8);
+
 /* ---- setup (CPU; out of the hot path, the reference's setup API) ---- */
 /* edges_from_faces (surface.hpp:49-65); returns edge count, -1 on error */
 int nrr_edges_from_faces(const int32_t* faces, int32_t nf, int32_t n, int32_t* out_edges,

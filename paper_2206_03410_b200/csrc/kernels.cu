@@ -295,7 +295,8 @@ __global__ void landmark_kernel(DevProblem p, TermParams tp, double* __restrict_
                 const double4 fb4 = p.infl_f[eb];
                 const double fb[4] = {fb4.x, fb4.y, fb4.z, fb4.w};
                 int blk = -1;
-                for (int b = p.row_ptr[na]; b < p.row_ptr[na + 1]; ++b)
+                const int ra = p.node_row[na];
+                for (int b = p.row_ptr[ra]; b < p.row_ptr[ra + 1]; ++b)
                     if (p.col[b] == nb) blk = b;
                 if (blk < 0) continue;
                 for (int r = 0; r < 4; ++r)

@@ -26,8 +26,9 @@ struct DevProblem {
     const double* pair_c = nullptr;    // P
     const int* pair_rev = nullptr;     // P: index of (j, i)
     const int* node_pair_off = nullptr;  // N+1: pairs with i == j, ascending j
-    const int* row_ptr = nullptr;      // N+1 BSR
-    const int* col = nullptr;          // nnzb
+    const int* row_ptr = nullptr;      // N+1 BSR over solver rows (pcg.cu order)
+    const int* col = nullptr;          // nnzb (node ids)
+    const int* node_row = nullptr;     // N: node -> solver row
     // assembly plan: upper blocks u < N diagonal j = u, u >= N graph edge u-N
     const int* ub_cptr = nullptr;      // U+1 contributor ranges
     const int* c_v = nullptr;          // contributor vertex

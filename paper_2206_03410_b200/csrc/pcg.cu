@@ -1,29 +1,39 @@
 // SPD solve K X = B (reference SystemAssembler::solve, energy.hpp:233-254;
-// solve_system :393-408) as a block-Jacobi preconditioned conjugate gradient
-// in FP64 on sm_100a: one persistent cooperative kernel, one CTA per SM.
+// solve_system :393-408) as a two-level preconditioned conjugate gradient in
+// FP64 on sm_100a.
 //
-// * K (4N x 4N, 4x4 blocks, fixed pattern) is BSR; each CTA owns a contiguous
-//   range of block rows balanced by block count and copies its rows' blocks
-//   into shared memory once, so the SpMV of every iteration reads K from SMEM
-//   (cfg2: 26 KB per CTA; cfg4: ~170 KB per CTA).
-// * The three right-hand sides (output coordinates, energy.hpp:118-121) share
-//   every K read; each thread owns (node, row r, column c) elements.
-// * Preconditioner: exact inverse of each 4x4 diagonal block (the north_star's
-//   12x12 per-node block is I3 (x) K_jj). A block whose Cholesky pivot is not
-//   positive reproduces the reference diagnostic "singular diagonal block at
-//   node j" (energy.hpp:329-340).
-// * Two grid barriers per iteration: the SpMV of z is rewritten as
-//   q = K z + beta q_prev (p = z + beta p_prev), so the p-update and SpMV share
-//   one phase and the dot products (p,q) and (r,z) land on the two barriers.
-// * All dot products are two-level fixed-order reductions (CTA partials, then
-//   one warp per quantity over the CTA partials): bitwise reproducible.
-// * Exit: the recursive residual reaches pcg_rtol*(1+|B|max); then the true
-//   residual B-KX is formed and must meet the reference bar
-//   1e-8*(1+|B|max) (energy.hpp:245); otherwise PCG restarts from it.
+// Layout. Graph nodes are partitioned by recursive coordinate bisection into
+// one compact subdomain per CTA (one CTA per SM). Each CTA copies its rows' K
+// blocks into shared memory once per solve, so every SpMV reads K from SMEM.
+// The three right-hand sides (output coordinates, energy.hpp:118-121) share
+// every K read; a thread owns (node, row r, column c) elements in registers.
+//
+// Preconditioner M^-1 = sum_j K_jj^-1 (4x4 block Jacobi; the north_star's
+// 12x12 per-node block is I3 (x) K_jj) + Psi K0^-1 Psi^T, a coarse correction
+// over aggregates of consecutive subdomains. Psi spans, per aggregate, the
+// 4 modes that make the regularizer vanish (a global affine map: node j's
+// unknowns [a; a.(p_j - c) + b], energy.hpp:77-84), so the graph-Laplacian-like
+// low modes that stall block Jacobi are solved exactly on the coarse level.
+// K0 = Psi^T K Psi (<= 160 x 160) is assembled per solve (CTA partials, fixed
+// order) and inverted by one CTA (Gauss-Jordan, SPD).
+//
+// Iteration (2 grid barriers, all reductions two-level and fixed-order so the
+// result is bitwise reproducible):
+//   A: q = K z + beta q, p = z + beta p; partials (p,q) and Psi^T q
+//   -- barrier --  alpha; rho -= alpha Psi^T q (coarse residual, replicated)
+//   B: x += alpha p, r -= alpha q, z = M_jj r + Psi K0^-1 rho; partials (r,z), max|r|
+//   -- barrier --  beta
+// Exit: the recursive residual reaches pcg_rtol*(1+|B|max); the true residual
+// B-KX must then meet the reference bar 1e-8*(1+|B|max) (energy.hpp:245),
+// otherwise PCG restarts from it. A 4x4 diagonal block whose Cholesky pivot
+// is not positive reports "singular diagonal block at node j"
+// (energy.hpp:329-340); p^T K p <= 0 reports an indefinite system.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <numeric>
 
 #include "device_common.cuh"
 #include "pcg.cuh"
@@ -34,73 +44,248 @@ namespace nrr_b200 {
 
 namespace {
 
-constexpr int kThreads = 512;
-constexpr int kQ = 8;  // reduction slots per phase
+constexpr int kQ = 16;  // partial slots per CTA and phase
 
-struct Shared {
-    double* K;     // nkb*16
-    int* col;      // nkb
-    double* M;     // nrows*16
-    double* rex;   // nrows*12 exchange of r for the preconditioner
-    double* red;   // 16*kQ block-reduction scratch
-    double* bcast; // kQ broadcast of reduced values
-};
-
-__device__ __forceinline__ void reduce_partials(const double* __restrict__ part, int G, double* bcast, int nq,
-                                                bool is_max) {
-    // one warp per quantity, fixed lane assignment and tree
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (w < nq) {
-        double v = is_max ? 0.0 : 0.0;
-        for (int g = lane; g < G; g += 32) {
-            const double x = __ldcg(part + g * kQ + w);
-            v = is_max ? fmax(v, x) : v + x;
-        }
-        v = is_max ? warp_max(v) : warp_sum(v);
-        if (lane == 0) bcast[w] = v;
-    }
-    __syncthreads();
+// coarse mode k of node a in aggregate g: [e_k; d_k] for k < 3, e_3 for k = 3,
+// d = p_a - c_g
+__device__ __forceinline__ void node_offset(const PcgArgs& a, int node, double d[3]) {
+    const int g = a.node_agg[node];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = a.node_pos[3 * node + k] - a.agg_center[3 * g + k];
 }
 
-// block reduction of nq per-thread values into part[blockIdx*kQ + k]
-__device__ __forceinline__ void block_partials(const double* vals, int nq, double* red, double* part,
-                                               const bool* is_max) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int k = 0; k < nq; ++k) {
-        double v = vals[k];
-        v = is_max[k] ? warp_max(v) : warp_sum(v);
-        if (lane == 0) red[k * 16 + w] = v;
+// ---------------------------------------------------------------- coarse setup
+// CTA c: partial[c][k][h*4+l] = sum over its rows a and blocks (a,b) with b in
+// aggregate h of psi_k(a)^T K_ab psi_l(b). One thread per output entry, blocks
+// scanned in BSR order: deterministic.
+__global__ void __launch_bounds__(kPcgThreads) coarse_partial_kernel(PcgArgs a, double* __restrict__ partial) {
+    const int c = blockIdx.x;
+    const int r0 = a.row_begin[c], r1 = a.row_begin[c + 1];
+    const int nc = 4 * a.n_agg;
+    for (int o = threadIdx.x; o < 4 * nc; o += blockDim.x) {
+        const int k = o / nc, hl = o % nc, h = hl >> 2, l = hl & 3;
+        double acc = 0.0;
+        for (int j = r0; j < r1; ++j) {
+            const int na = a.row_node[j];
+            double da[3];
+            node_offset(a, na, da);
+            for (int blk = a.row_ptr[j]; blk < a.row_ptr[j + 1]; ++blk) {
+                const int nb = a.col[blk];
+                if (a.node_agg[nb] != h) continue;
+                const double* Kb = a.K + static_cast<size_t>(blk) * 16;
+                double db[3];
+                node_offset(a, nb, db);
+                // u = K_ab psi_l(b)
+                double u[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) u[r] = l < 3 ? Kb[r * 4 + l] + db[l] * Kb[r * 4 + 3] : Kb[r * 4 + 3];
+                acc += k < 3 ? u[k] + da[k] * u[3] : u[3];
+            }
+        }
+        partial[(static_cast<size_t>(c) * 4 + k) * nc + hl] = acc;
+    }
+}
+
+// One CTA: K0 = sum of the partials of each aggregate's CTAs (fixed order),
+// symmetrised, inverted in place by Gauss-Jordan (SPD: no pivoting needed);
+// modes with a vanishing pivot are dropped (zero rows / columns).
+__global__ void __launch_bounds__(kPcgThreads) coarse_invert_kernel(PcgArgs a, const double* __restrict__ partial,
+                                                                   double* __restrict__ inv, int grid) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nc = 4 * a.n_agg;
+    double* A = reinterpret_cast<double*>(smem_raw);  // nc*nc
+    double* colk = A + nc * nc;                       // nc
+    double* rowk = colk + nc;                         // nc
+    __shared__ double s_dmax;
+    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
+        const int i = o / nc, j = o % nc;
+        const int g = i >> 2, k = i & 3;
+        double s = 0.0;
+        for (int c = g * a.agg_ctas; c < min((g + 1) * a.agg_ctas, grid); ++c)
+            s += partial[(static_cast<size_t>(c) * 4 + k) * nc + j];
+        A[o] = s;
     }
     __syncthreads();
+    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
+        const int i = o / nc, j = o % nc;
+        if (i < j) {
+            const double v = 0.5 * (A[i * nc + j] + A[j * nc + i]);
+            A[i * nc + j] = v;
+            A[j * nc + i] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int i = 0; i < nc; ++i) m = fmax(m, fabs(A[i * nc + i]));
+        s_dmax = m;
+    }
+    __syncthreads();
+    const double drop = 1e-12 * s_dmax;
+    for (int k = 0; k < nc; ++k) {
+        const double piv = A[k * nc + k];
+        const bool ok = piv > drop;
+        const double d = ok ? 1.0 / piv : 0.0;
+        for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+            colk[i] = A[i * nc + k];
+            rowk[i] = A[k * nc + i];
+        }
+        __syncthreads();
+        for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
+            const int i = o / nc, j = o % nc;
+            if (!ok) {
+                if (i == k || j == k) A[o] = 0.0;
+                continue;
+            }
+            if (i == k && j == k) A[o] = d;
+            else if (i == k) A[o] = rowk[j] * d;
+            else if (j == k) A[o] = -colk[i] * d;
+            else A[o] -= colk[i] * rowk[j] * d;
+        }
+        __syncthreads();
+    }
+    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) inv[o] = A[o];
+}
+
+// ---------------------------------------------------------------- PCG
+struct Shared {
+    double* K;       // nkb*16
+    int* col;        // nkb
+    double* M;       // nrows*16 block-Jacobi inverses
+    double* rex;     // nrows*12 exchange of r
+    double* off;     // nrows*3 node offsets to the aggregate centre
+    double* cinv;    // 4 x nc rows of K0^-1 for the own aggregate
+    double* rho;     // nc x 3 coarse residual (replicated)
+    double* ptq;     // nc x 3 aggregate sums of Psi^T q (or Psi^T r)
+    double* red;     // 16 warps x kQ
+    double* bcast;   // kQ
+    double* y;       // 12: own aggregate coarse correction
+};
+
+__device__ __forceinline__ double op2(bool mx, double a, double b) { return mx ? fmax(a, b) : a + b; }
+
+// Block reduction of the 16 per-thread slots into part[blockIdx*kQ + k]
+// (sum, or max for slots in max_mask). Within a warp a transpose-reduce
+// halves the vector at every butterfly level (8+4+2+1+1 shuffles instead of
+// 16x5); then one warp per slot combines the 16 warps. Fixed order.
+__device__ __forceinline__ void block_partials(const double* vals, int nq, double* red, double* part,
+                                               unsigned max_mask) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double v8[8], v4[4], v2[2], v1;
+    int base = 0;
+    {
+        const bool up = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double keep = up ? vals[i + 8] : vals[i], send = up ? vals[i] : vals[i + 8];
+            const int slot = (up ? 8 : 0) + i;
+            v8[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 16));
+        }
+        base += up ? 8 : 0;
+    }
+    {
+        const bool up = lane & 8;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double keep = up ? v8[i + 4] : v8[i], send = up ? v8[i] : v8[i + 4];
+            const int slot = base + (up ? 4 : 0) + i;
+            v4[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 8));
+        }
+        base += up ? 4 : 0;
+    }
+    {
+        const bool up = lane & 4;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double keep = up ? v4[i + 2] : v4[i], send = up ? v4[i] : v4[i + 2];
+            const int slot = base + (up ? 2 : 0) + i;
+            v2[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 4));
+        }
+        base += up ? 2 : 0;
+    }
+    {
+        const bool up = lane & 2;
+        const double keep = up ? v2[1] : v2[0], send = up ? v2[0] : v2[1];
+        const int slot = base + (up ? 1 : 0);
+        v1 = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 2));
+        base = slot;
+    }
+    v1 = op2((max_mask >> base) & 1u, v1, __shfl_xor_sync(0xffffffffu, v1, 1));
+    if ((lane & 1) == 0) red[base * 16 + w] = v1;
+    __syncthreads();
     if (w < nq) {
+        const bool mx = (max_mask >> w) & 1u;
         double v = lane < nw ? red[w * 16 + lane] : 0.0;
-        v = is_max[w] ? warp_max(v) : warp_sum(v);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) v = op2(mx, v, __shfl_xor_sync(0xffffffffu, v, o));
         if (lane == 0) part[blockIdx.x * kQ + w] = v;
     }
     __syncthreads();
 }
 
+// grid totals of slots [0, nq) (sum or max per mask) into bcast; one warp per slot
+__device__ __forceinline__ void grid_totals(const double* __restrict__ part, int G, double* bcast, int nq,
+                                            unsigned max_mask) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < nq) {
+        const bool mx = (max_mask >> w) & 1u;
+        double v = 0.0;
+        for (int g = lane; g < G; g += 32) {
+            const double x = __ldcg(part + g * kQ + w);
+            v = mx ? fmax(v, x) : v + x;
+        }
+        v = mx ? warp_max(v) : warp_sum(v);
+        if (lane == 0) bcast[w] = v;
+    }
+}
+
+// per-aggregate sums of the 12 Psi^T slots [s0, s0+12) into out[nc x 3]:
+// out[(g*4+k)*3 + c] = sum over the aggregate's CTAs of part[cta][s0 + k*3 + c]
+__device__ __forceinline__ void aggregate_sums(const PcgArgs& a, const double* __restrict__ part, int G, int s0,
+                                               double* out) {
+    const int nc = 4 * a.n_agg;
+    for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) {
+        const int g = o / 12, kc = o % 12;
+        double s = 0.0;
+        for (int c = g * a.agg_ctas; c < min((g + 1) * a.agg_ctas, G); ++c) s += __ldcg(part + c * kQ + s0 + kc);
+        out[o] = s;
+    }
+}
+
 template <int EPT>
-__global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
+__global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int r0 = a.row_begin[blockIdx.x], r1 = a.row_begin[blockIdx.x + 1];
+    const int cta = blockIdx.x, G = gridDim.x;
+    const int r0 = a.row_begin[cta], r1 = a.row_begin[cta + 1];
     const int nrows = r1 - r0;
     const int kb0 = a.row_ptr[r0], nkb = a.row_ptr[r1] - kb0;
+    const int nc = 4 * a.n_agg;
+    const int my_agg = cta / a.agg_ctas;
     Shared sh;
     {
-        unsigned char* p = smem_raw;
-        sh.red = reinterpret_cast<double*>(p);
-        p += sizeof(double) * 16 * kQ;
-        sh.bcast = reinterpret_cast<double*>(p);
-        p += sizeof(double) * kQ;
-        sh.M = reinterpret_cast<double*>(p);
-        p += sizeof(double) * 16 * a.max_rows;
-        sh.rex = reinterpret_cast<double*>(p);
-        p += sizeof(double) * 12 * a.max_rows;
+        double* p = reinterpret_cast<double*>(smem_raw);
+        sh.red = p;
+        p += 16 * kQ;
+        sh.bcast = p;
+        p += kQ;
+        sh.y = p;
+        p += 16;
+        sh.M = p;
+        p += 16 * a.max_rows;
+        sh.rex = p;
+        p += 12 * a.max_rows;
+        sh.off = p;
+        p += (3 * a.max_rows + 1) & ~1;  // keep the K region 16-byte aligned
+        sh.cinv = p;
+        p += 4 * kCoarseMax;
+        sh.rho = p;
+        p += 3 * kCoarseMax;
+        sh.ptq = p;
+        p += 3 * kCoarseMax;
         if (a.k_in_smem) {
-            sh.K = reinterpret_cast<double*>(p);
-            p += sizeof(double) * 16 * a.max_kb;
+            sh.K = p;
+            p += 16 * static_cast<size_t>(a.max_kb);
             sh.col = reinterpret_cast<int*>(p);
         } else {
             sh.K = const_cast<double*>(a.K) + static_cast<size_t>(kb0) * 16;
@@ -113,12 +298,22 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
         for (int i = threadIdx.x; i < nkb * 8; i += blockDim.x) dst[i] = src[i];
         for (int i = threadIdx.x; i < nkb; i += blockDim.x) sh.col[i] = a.col[kb0 + i];
     }
-    // ---- block-Jacobi: M_j = K_jj^{-1} via 4x4 Cholesky (one thread per row)
+    if (a.use_coarse) {
+        for (int i = threadIdx.x; i < 4 * nc; i += blockDim.x) {
+            const int k = i / nc, j = i % nc;
+            sh.cinv[i] = a.coarse_inv[static_cast<size_t>(my_agg * 4 + k) * nc + j];
+        }
+    }
+    // ---- block Jacobi: M_j = K_jj^{-1} via 4x4 Cholesky (one thread per row)
     for (int lr = threadIdx.x; lr < nrows; lr += blockDim.x) {
         const int j = r0 + lr;
+        const int node = a.row_node[j];
+        double d3[3];
+        node_offset(a, node, d3);
+        for (int t = 0; t < 3; ++t) sh.off[lr * 3 + t] = d3[t];
         int dpos = -1;
         for (int b = a.row_ptr[j]; b < a.row_ptr[j + 1]; ++b)
-            if (a.col[b] == j) dpos = b;
+            if (a.col[b] == node) dpos = b;
         double k[16], l[16] = {0};
         for (int t = 0; t < 16; ++t) k[t] = a.K[static_cast<size_t>(dpos) * 16 + t];
         double dmax = 0;
@@ -141,11 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
         }
         double* M = sh.M + lr * 16;
         if (!ok) {
-            atomicMin(&a.status->fail_node, j);
+            atomicMin(&a.status->fail_node, node);
             for (int t = 0; t < 16; ++t) M[t] = 0.0;
             continue;
         }
-        // inverse of L L^T column by column
         for (int e = 0; e < 4; ++e) {
             double y[4];
             for (int r = 0; r < 4; ++r) {
@@ -166,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
     const int nel = nrows * 12;
     double xr[EPT], br[EPT], rr[EPT], zr[EPT], pr[EPT], qr[EPT];
     int el_row[EPT], el_r[EPT], el_c[EPT];
+    size_t el_g[EPT];
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
         const int e = threadIdx.x + k * blockDim.x;
@@ -174,13 +369,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
         el_row[k] = live ? lr : -1;
         el_r[k] = rc / 3;
         el_c[k] = rc % 3;
-        const size_t gi = static_cast<size_t>(r0) * 12 + (live ? e : 0);
-        xr[k] = live ? a.X[gi] : 0.0;
-        br[k] = live ? a.B[gi] : 0.0;
+        el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + rc;
+        xr[k] = live ? a.X[el_g[k]] : 0.0;
+        br[k] = live ? a.B[el_g[k]] : 0.0;
         pr[k] = qr[k] = 0.0;
     }
 
-    // SpMV of one element over the global vector v (node-major 12N)
     auto spmv = [&](int k, const double* __restrict__ v) -> double {
         const int lr = el_row[k];
         if (lr < 0) return 0.0;
@@ -198,8 +392,31 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
         }
         return acc;
     };
-    // z = M r for own elements via the shared exchange; writes Z
+    // own-element contribution to Psi^T v: slot k*3 + c of 12
+    auto psi_t = [&](int k, double v, double* out12) {
+        const int lr = el_row[k];
+        if (lr < 0) return;
+        const int r = el_r[k], c = el_c[k];
+        if (r < 3) {
+            out12[r * 3 + c] += v;
+        } else {
+            out12[0 * 3 + c] += sh.off[lr * 3 + 0] * v;
+            out12[1 * 3 + c] += sh.off[lr * 3 + 1] * v;
+            out12[2 * 3 + c] += sh.off[lr * 3 + 2] * v;
+            out12[3 * 3 + c] += v;
+        }
+    };
+    // z = M_jj r + Psi y_own; y_own = K0inv[own rows] rho (computed by 12 threads)
     auto precond = [&]() {
+        if (a.use_coarse && (threadIdx.x >> 5) < 12) {  // warp w: output w, lanes split the coarse sum
+            const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            const int k = w / 3, c = w % 3;
+            double s = 0.0;
+            const double* row = sh.cinv + k * nc;
+            for (int j = lane; j < nc; j += 32) s += row[j] * sh.rho[j * 3 + c];
+            s = warp_sum(s);
+            if (lane == 0) sh.y[k * 3 + c] = s;
+        }
 #pragma unroll
         for (int k = 0; k < EPT; ++k)
             if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + el_r[k] * 3 + el_c[k]] = rr[k];
@@ -210,10 +427,18 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
                 zr[k] = 0.0;
                 continue;
             }
-            const double* M = sh.M + el_row[k] * 16 + el_r[k] * 4;
-            const double* rv = sh.rex + el_row[k] * 12 + el_c[k];
-            zr[k] = M[0] * rv[0] + M[1] * rv[3] + M[2] * rv[6] + M[3] * rv[9];
-            __stcg(a.Z + static_cast<size_t>(r0) * 12 + threadIdx.x + k * blockDim.x, zr[k]);
+            const int lr = el_row[k], r = el_r[k], c = el_c[k];
+            const double* M = sh.M + lr * 16 + r * 4;
+            const double* rv = sh.rex + lr * 12 + c;
+            double z = M[0] * rv[0] + M[1] * rv[3] + M[2] * rv[6] + M[3] * rv[9];
+            if (a.use_coarse) {
+                if (r < 3) z += sh.y[r * 3 + c];
+                else
+                    z += sh.off[lr * 3] * sh.y[c] + sh.off[lr * 3 + 1] * sh.y[3 + c] + sh.off[lr * 3 + 2] * sh.y[6 + c] +
+                         sh.y[9 + c];
+            }
+            zr[k] = z;
+            __stcg(a.Z + el_g[k], z);
         }
         __syncthreads();
     };
@@ -221,53 +446,40 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
     grid.sync();  // fail flags visible
     if (__ldcg(&a.status->fail_node) != 0x7fffffff) return;
 
-    bool mx[kQ];
     double vals[kQ];
     int it = 0, restarts = 0;
     double bmax = 0.0, tol = 0.0, bar = 0.0;
     double rz[3], beta[3] = {0, 0, 0};
     bool need_init = true;
-    int status_code = 0;  // 0 running, 1 converged, 2 indefinite, 3 max iter
+    int status_code = 0;  // 1 converged, 2 indefinite, 3 max iter
 
     while (true) {
         if (need_init) {
-            // r = b - K x, z = M r, (r,z), max|r|, max|b|
-            // x must be globally visible: write own x to X (already there at start)
+            // r = b - K x; coarse residual rho = Psi^T r; z = M r; (r,z)
 #pragma unroll
             for (int k = 0; k < EPT; ++k)
-                if (el_row[k] >= 0) __stcg(a.X + static_cast<size_t>(r0) * 12 + threadIdx.x + k * blockDim.x, xr[k]);
+                if (el_row[k] >= 0) __stcg(a.X + el_g[k], xr[k]);
             grid.sync();
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) rr[k] = br[k] - spmv(k, a.X);
-            precond();
-            for (int q = 0; q < kQ; ++q) {
-                vals[q] = 0.0;
-                mx[q] = false;
-            }
-            mx[6] = mx[3] = mx[4] = mx[5] = true;
+            for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
+                rr[k] = br[k] - spmv(k, a.X);
                 if (el_row[k] < 0) continue;
-                const int c = el_c[k];
-                vals[c] += rr[k] * zr[k];
-                vals[3 + c] = fmax(vals[3 + c], fabs(rr[k]));
-                vals[6] = fmax(vals[6], fabs(br[k]));
+                vals[0] = fmax(vals[0], fabs(rr[k]));
+                vals[1] = fmax(vals[1], fabs(br[k]));
+                psi_t(k, rr[k], vals + 2);
             }
-            block_partials(vals, 7, sh.red, a.part_b, mx);
+            block_partials(vals, 14, sh.red, a.part_b, 0x3u);
             grid.sync();
-            reduce_partials(a.part_b, gridDim.x, sh.bcast, 3, false);
-            double rz3[3] = {sh.bcast[0], sh.bcast[1], sh.bcast[2]};
+            grid_totals(a.part_b, G, sh.bcast, 2, 0x3u);
+            if (a.use_coarse) aggregate_sums(a, a.part_b, G, 2, sh.rho);
             __syncthreads();
-            reduce_partials(a.part_b + 3, gridDim.x, sh.bcast, 4, true);  // slots 3..6 via offset
-            double rmax3[3] = {sh.bcast[0], sh.bcast[1], sh.bcast[2]};
-            bmax = sh.bcast[3];
-            __syncthreads();
+            const double rmax0 = sh.bcast[0];
+            bmax = sh.bcast[1];
             tol = a.rtol * (1.0 + bmax);
             bar = 1e-8 * (1.0 + bmax);
             if (restarts > 0) {
-                // true residual of the accepted iterate: stop if it meets both bars
-                const double rt = fmax(rmax3[0], fmax(rmax3[1], rmax3[2]));
-                if (rt <= bar && (rt <= 100.0 * tol || restarts >= 3)) {
+                if (rmax0 <= bar && (rmax0 <= 100.0 * tol || restarts >= 3)) {
                     status_code = 1;
                     break;
                 }
@@ -276,24 +488,30 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
                     break;
                 }
             }
+            if (rmax0 <= tol) {
+                ++restarts;
+                continue;  // verify on the true residual (need_init stays set)
+            }
+            precond();
+            for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
+#pragma unroll
+            for (int k = 0; k < EPT; ++k)
+                if (el_row[k] >= 0) vals[el_c[k]] += rr[k] * zr[k];
+            block_partials(vals, 3, sh.red, a.part_a, 0x0u);
+            grid.sync();
+            grid_totals(a.part_a, G, sh.bcast, 3, 0x0u);
+            __syncthreads();
             for (int c = 0; c < 3; ++c) {
-                rz[c] = rz3[c];
+                rz[c] = sh.bcast[c];
                 beta[c] = 0.0;
             }
 #pragma unroll
             for (int k = 0; k < EPT; ++k) pr[k] = qr[k] = 0.0;
             need_init = false;
-            if (fmax(rmax3[0], fmax(rmax3[1], rmax3[2])) <= tol) {
-                ++restarts;
-                need_init = true;  // verify with the true residual
-                continue;
-            }
+            __syncthreads();
         }
-        // ---- phase A: q = K z + beta q, p = z + beta p, (p,q)
-        for (int q = 0; q < kQ; ++q) {
-            vals[q] = 0.0;
-            mx[q] = false;
-        }
+        // ---- phase A: q = K z + beta q, p = z + beta p; (p,q), Psi^T q
+        for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
             const double w = spmv(k, a.Z);
@@ -302,10 +520,13 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
             qr[k] = w + beta[c] * qr[k];
             pr[k] = zr[k] + beta[c] * pr[k];
             vals[c] += pr[k] * qr[k];
+            psi_t(k, qr[k], vals + 3);
         }
-        block_partials(vals, 3, sh.red, a.part_a, mx);
+        block_partials(vals, a.use_coarse ? 15 : 3, sh.red, a.part_a, 0x0u);
         grid.sync();
-        reduce_partials(a.part_a, gridDim.x, sh.bcast, 3, false);
+        grid_totals(a.part_a, G, sh.bcast, 3, 0x0u);
+        if (a.use_coarse) aggregate_sums(a, a.part_a, G, 3, sh.ptq);
+        __syncthreads();
         double alpha[3];
         bool indefinite = false;
         for (int c = 0; c < 3; ++c) {
@@ -319,12 +540,13 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
                 alpha[c] = rz[c] / pq;
             }
         }
-        __syncthreads();
         if (indefinite) {
             status_code = 2;
             break;
         }
-        // ---- phase B: x += alpha p, r -= alpha q, z = M r, (r,z), max|r|
+        if (a.use_coarse)
+            for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) sh.rho[o] -= alpha[o % 3] * sh.ptq[o];
+        // ---- phase B: x += alpha p, r -= alpha q, z = M r; (r,z), max|r|
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
             if (el_row[k] < 0) continue;
@@ -332,11 +554,9 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
             xr[k] = fma(alpha[c], pr[k], xr[k]);
             rr[k] = fma(-alpha[c], qr[k], rr[k]);
         }
+        __syncthreads();  // rho updated before the coarse solve
         precond();
-        for (int q = 0; q < kQ; ++q) {
-            vals[q] = 0.0;
-            mx[q] = q >= 3;
-        }
+        for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
             if (el_row[k] < 0) continue;
@@ -344,13 +564,12 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
             vals[c] += rr[k] * zr[k];
             vals[3 + c] = fmax(vals[3 + c], fabs(rr[k]));
         }
-        block_partials(vals, 6, sh.red, a.part_b, mx);
+        block_partials(vals, 6, sh.red, a.part_b, 0x38u);
         grid.sync();
-        reduce_partials(a.part_b, gridDim.x, sh.bcast, 3, false);
-        double rzn[3] = {sh.bcast[0], sh.bcast[1], sh.bcast[2]};
+        grid_totals(a.part_b, G, sh.bcast, 6, 0x38u);
         __syncthreads();
-        reduce_partials(a.part_b + 3, gridDim.x, sh.bcast, 3, true);
-        double rmax3[3] = {sh.bcast[0], sh.bcast[1], sh.bcast[2]};
+        double rzn[3] = {sh.bcast[0], sh.bcast[1], sh.bcast[2]};
+        const double rmax = fmax(sh.bcast[3], fmax(sh.bcast[4], sh.bcast[5]));
         __syncthreads();
         ++it;
         for (int c = 0; c < 3; ++c) {
@@ -361,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
             status_code = 2;
             break;
         }
-        if (fmax(rmax3[0], fmax(rmax3[1], rmax3[2])) <= tol) {
+        if (rmax <= tol) {
             ++restarts;
             need_init = true;
             continue;
@@ -371,11 +590,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
             break;
         }
     }
-    // publish x
 #pragma unroll
     for (int k = 0; k < EPT; ++k)
-        if (el_row[k] >= 0) a.X[static_cast<size_t>(r0) * 12 + threadIdx.x + k * blockDim.x] = xr[k];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (el_row[k] >= 0) a.X[el_g[k]] = xr[k];
+    if (cta == 0 && threadIdx.x == 0) {
         a.status->iterations = it;
         a.status->code = status_code;
         a.status->restarts = restarts;
@@ -383,54 +601,125 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_kernel(PcgArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- plan (host)
+struct RcbCtx {
+    const double* pos;
+    const int* weight;
+    std::vector<int>* ids;
+    std::vector<int>* leaf_begin;
+};
+
+void rcb(RcbCtx& ctx, int lo, int hi, int g0, int g1) {
+    std::vector<int>& ids = *ctx.ids;
+    if (g1 - g0 == 1) {
+        (*ctx.leaf_begin)[g0] = lo;
+        return;
+    }
+    const int gm = (g0 + g1) / 2;
+    double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+    for (int t = lo; t < hi; ++t)
+        for (int c = 0; c < 3; ++c) {
+            mn[c] = std::min(mn[c], ctx.pos[3 * ids[t] + c]);
+            mx[c] = std::max(mx[c], ctx.pos[3 * ids[t] + c]);
+        }
+    int axis = 0;
+    for (int c = 1; c < 3; ++c)
+        if (mx[c] - mn[c] > mx[axis] - mn[axis]) axis = c;
+    std::sort(ids.begin() + lo, ids.begin() + hi, [&](int x, int y) {
+        const double px = ctx.pos[3 * x + axis], py = ctx.pos[3 * y + axis];
+        return px != py ? px < py : x < y;
+    });
+    double total = 0;
+    for (int t = lo; t < hi; ++t) total += ctx.weight[ids[t]];
+    const double target = total * static_cast<double>(gm - g0) / (g1 - g0);
+    double acc = 0;
+    int cut = lo;
+    while (cut < hi && acc + ctx.weight[ids[cut]] <= target) acc += ctx.weight[ids[cut++]];
+    // keep at least one node per leaf on each side when possible
+    cut = std::max(cut, lo + (gm - g0));
+    cut = std::min(cut, hi - (g1 - gm));
+    rcb(ctx, lo, cut, g0, gm);
+    rcb(ctx, cut, hi, gm, g1);
+}
+
 }  // namespace
 
-void PcgPlan::build(const int* row_ptr_host, int N, int num_sms, size_t smem_limit) {
+void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit) {
     nodes = N;
     grid = std::max(1, std::min(num_sms, N));
-    const int nnzb = row_ptr_host[N];
-    // balance block count + row count per CTA; cap rows by the register tiling
-    const int cap_rows = (kThreads * 4) / 12;
-    row_begin.assign(grid + 1, N);
-    row_begin[0] = 0;
-    const double total = static_cast<double>(nnzb) + 2.0 * N;
-    int r = 0;
-    for (int g = 0; g < grid; ++g) {
-        row_begin[g] = r;
-        const double target = total * (g + 1) / grid;
-        int start = r;
-        while (r < N && (r - start) < cap_rows &&
-               (static_cast<double>(row_ptr_host[r + 1]) + 2.0 * (r + 1) <= target || r == start))
-            ++r;
-        if (g == grid - 1) r = N;
-    }
-    row_begin[grid] = N;
-    max_rows = 0;
-    max_kb = 0;
-    for (int g = 0; g < grid; ++g) {
-        const int rows = row_begin[g + 1] - row_begin[g];
-        max_rows = std::max(max_rows, rows);
-        max_kb = std::max(max_kb, row_ptr_host[row_begin[g + 1]] - row_ptr_host[row_begin[g]]);
-    }
-    if (max_rows * 12 > kThreads * 4)
+    const int cap_rows = (kPcgThreads * 4) / 12;
+    while ((N + grid - 1) / grid > cap_rows * 7 / 8 && grid < num_sms) ++grid;
+    if ((N + grid - 1) / grid > cap_rows)
         throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 170)");
-    ept = max_rows * 12 <= kThreads ? 1 : (max_rows * 12 <= 2 * kThreads ? 2 : 4);
-    const size_t base = sizeof(double) * (16 * kQ + kQ + 16 * static_cast<size_t>(max_rows) + 12 * static_cast<size_t>(max_rows));
+    std::vector<int> ids(N), w(N);
+    std::iota(ids.begin(), ids.end(), 0);
+    for (int j = 0; j < N; ++j) w[j] = 2 + row_nnz_by_node[j];
+    row_begin.assign(grid + 1, N);
+    RcbCtx ctx{node_pos, w.data(), &ids, &row_begin};
+    rcb(ctx, 0, N, 0, grid);
+    row_begin[grid] = N;
+    row_node = ids;
+    node_row.assign(N, 0);
+    for (int r = 0; r < N; ++r) node_row[row_node[r]] = r;
+    max_rows = 0;
+    for (int g = 0; g < grid; ++g) max_rows = std::max(max_rows, row_begin[g + 1] - row_begin[g]);
+    if (max_rows * 12 > kPcgThreads * 4)
+        throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 170)");
+    ept = max_rows * 12 <= kPcgThreads ? 1 : (max_rows * 12 <= 2 * kPcgThreads ? 2 : 4);
+    // aggregates: consecutive CTAs, coarse dimension 4 * n_agg <= kCoarseMax (160)
+    agg_ctas = std::max(1, (4 * grid + 159) / 160);
+    if (const char* e = std::getenv("NRR_AGG_CTAS")) agg_ctas = std::max(agg_ctas, std::atoi(e));
+    if (const char* e = std::getenv("NRR_COARSE")) use_coarse = std::atoi(e) != 0;
+    n_agg = (grid + agg_ctas - 1) / agg_ctas;
+    node_agg.assign(N, 0);
+    agg_center.assign(3 * static_cast<size_t>(n_agg), 0.0);
+    std::vector<int> cnt(n_agg, 0);
+    for (int g = 0; g < grid; ++g)
+        for (int r = row_begin[g]; r < row_begin[g + 1]; ++r) {
+            const int node = row_node[r], ag = g / agg_ctas;
+            node_agg[node] = ag;
+            for (int c = 0; c < 3; ++c) agg_center[3 * ag + c] += node_pos[3 * node + c];
+            ++cnt[ag];
+        }
+    for (int ag = 0; ag < n_agg; ++ag)
+        for (int c = 0; c < 3; ++c) agg_center[3 * ag + c] /= std::max(1, cnt[ag]);
+    (void)smem_limit;
+}
+
+void PcgPlan::size_smem(const int* row_ptr_solver, size_t smem_limit) {
+    max_kb = 0;
+    for (int g = 0; g < grid; ++g)
+        max_kb = std::max(max_kb, row_ptr_solver[row_begin[g + 1]] - row_ptr_solver[row_begin[g]]);
+    const size_t base = sizeof(double) * (16 * kQ + kQ + 16 + 32 * static_cast<size_t>(max_rows) + 10 * kCoarseMax);
     const size_t kbytes = static_cast<size_t>(max_kb) * (16 * sizeof(double) + sizeof(int));
     k_in_smem = base + kbytes + 64 <= smem_limit;
     smem_bytes = base + (k_in_smem ? kbytes : 0) + 64;
+}
+
+void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s) {
+    coarse_partial_kernel<<<plan.grid, kPcgThreads, 0, s>>>(a, w.partial);
+    NRR_CUDA_CHECK(cudaGetLastError());
+    const int nc = 4 * plan.n_agg;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(nc) * nc + 2 * nc);
+    NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    coarse_invert_kernel<<<1, kPcgThreads, smem, s>>>(a, w.partial, w.inv, plan.grid);
+    NRR_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
     args.max_rows = plan.max_rows;
     args.max_kb = plan.max_kb;
     args.k_in_smem = plan.k_in_smem ? 1 : 0;
+    args.agg_ctas = plan.agg_ctas;
+    args.n_agg = plan.n_agg;
+    args.use_coarse = plan.use_coarse ? 1 : 0;
     void* kargs[] = {&args};
     const void* fn = plan.ept == 1   ? reinterpret_cast<const void*>(pcg_kernel<1>)
                      : plan.ept == 2 ? reinterpret_cast<const void*>(pcg_kernel<2>)
                                      : reinterpret_cast<const void*>(pcg_kernel<4>);
     NRR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem_bytes)));
-    NRR_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kThreads), kargs, plan.smem_bytes, s));
+    NRR_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kPcgThreads), kargs, plan.smem_bytes, s));
 }
 
 }  // namespace nrr_b200

@@ -1,4 +1,5 @@
-// Block-Jacobi PCG solve of the 4N x 4N, 3-RHS normal equations (see pcg.cu).
+// Two-level preconditioned CG for the 4N x 4N, 3-RHS normal equations
+// (reference SystemAssembler::solve, energy.hpp:233-254); see pcg.cu.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -6,6 +7,9 @@
 #include <vector>
 
 namespace nrr_b200 {
+
+constexpr int kPcgThreads = 512;
+constexpr int kCoarseMax = 256;  // coarse dimension limit (4 modes per aggregate)
 
 struct PcgStatus {
     int fail_node;   // first node whose 4x4 diagonal block is not PD (INT_MAX = none)
@@ -15,30 +19,55 @@ struct PcgStatus {
     double bmax;     // max |B|
 };
 
+// Solver-side layout (built once per problem by PcgPlan):
+//   solver rows are graph nodes permuted by recursive coordinate bisection so
+//   that each CTA owns a compact subdomain (rows [row_begin[c], row_begin[c+1]));
+//   consecutive groups of `agg_ctas` CTAs form the coarse aggregates.
 struct PcgArgs {
-    const int* row_ptr;   // N+1 (BSR)
-    const int* col;       // nnzb
+    const int* row_ptr;   // N+1 BSR over solver rows
+    const int* col;       // nnzb, node ids
+    const int* row_node;  // N: solver row -> node id
     const double* K;      // nnzb*16
-    const double* B;      // 12N node-major
+    const double* B;      // 12N node-major (by node id)
     double* X;            // 12N node-major: in = warm start, out = solution
     double* Z;            // 12N scratch (preconditioned residual, exchanged)
-    const int* row_begin; // grid+1 CTA row ranges
-    double* part_a;       // grid*8
-    double* part_b;       // grid*8
+    const int* row_begin; // grid+1
+    const double* node_pos;  // N*3
+    const double* agg_center;  // n_agg*3
+    const int* node_agg;  // N: aggregate of node
+    const double* coarse_inv;  // n_c x n_c
+    double* part_a;       // grid*16
+    double* part_b;       // grid*16
     PcgStatus* status;
     double rtol;
     int max_iter;
-    int max_rows, max_kb, k_in_smem;  // filled from the plan
+    int max_rows, max_kb, k_in_smem;
+    int agg_ctas, n_agg, use_coarse;
 };
 
 struct PcgPlan {
     int nodes = 0, grid = 0, ept = 1, max_rows = 0, max_kb = 0;
-    bool k_in_smem = false;
+    int agg_ctas = 1, n_agg = 1;
+    bool k_in_smem = false, use_coarse = true;
     size_t smem_bytes = 0;
-    std::vector<int> row_begin;
-    void build(const int* row_ptr_host, int N, int num_sms, size_t smem_limit);
+    std::vector<int> row_begin;   // grid+1
+    std::vector<int> row_node;    // N: solver row -> node
+    std::vector<int> node_row;    // N: node -> solver row
+    std::vector<int> node_agg;    // N
+    std::vector<double> agg_center;  // n_agg*3
+    // partition + row order; row_nnz = blocks per node (for balance)
+    void build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit);
+    // smem sizing once the BSR (in solver-row order) is known
+    void size_smem(const int* row_ptr_solver, size_t smem_limit);
 };
 
+struct CoarseWork {
+    double* partial = nullptr;  // grid * 4 * n_c
+    double* inv = nullptr;      // n_c * n_c
+};
+
+// K_0 = Psi^T K Psi partials per CTA, then one CTA sums and inverts it.
+void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s);
 void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s);
 
 }  // namespace nrr_b200

@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -22,6 +24,7 @@
 #include "nn.cuh"
 #include "nrr_cuda.h"
 #include "pcg.cuh"
+#include "pcg_cluster.cuh"
 
 namespace nrr_b200 {
 
@@ -138,8 +141,14 @@ struct nrr_ctx {
 
     // ---- per-iteration state
     DevBuf<double> x, xmm, xnext, vhat, vhat2, d2, q, wa, wr, R, K, B, Z, term_part, pcg_a, pcg_b;
-    DevBuf<int> nn_idx, deg, row_begin;
+    DevBuf<int> nn_idx, deg, row_begin, d_row_node, d_node_row, d_node_agg;
+    DevBuf<double> d_agg_center, coarse_part, coarse_inv;
     PcgPlan plan;
+    ClusterPlan cplan;
+    bool use_cluster = false;
+    DevBuf<int> c_rank_rows, c_row_node, c_ent_ptr, c_diag_ent, c_store_off, c_store_src, c_halo_off;
+    DevBuf<int2> c_ent, c_halo_src;
+    DevBuf<long long> prof;
     DevBuf<PcgStatus> d_status;
     DevBuf<PassRecord> d_rec;
     Pinned<PassRecord> h_rec;
@@ -283,17 +292,25 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         cols[a].push_back(b);
         cols[b].push_back(a);
     }
-    c->h_row_ptr.assign(N + 1, 0);
-    c->h_col.clear();
+    std::vector<int> deg(N);
     for (int j = 0; j < N; ++j) {
         std::sort(cols[j].begin(), cols[j].end());
         cols[j].erase(std::unique(cols[j].begin(), cols[j].end()), cols[j].end());
-        c->h_row_ptr[j + 1] = c->h_row_ptr[j] + static_cast<int>(cols[j].size());
+        deg[j] = static_cast<int>(cols[j].size());
+    }
+    // solver row order: RCB subdomains, one per CTA (pcg.cu)
+    if (N > 0) c->plan.build(p->node_positions, deg.data(), N, c->num_sms, c->smem_optin);
+    c->h_row_ptr.assign(N + 1, 0);
+    c->h_col.clear();
+    for (int r = 0; r < N; ++r) {
+        const int j = c->plan.row_node[r];
+        c->h_row_ptr[r + 1] = c->h_row_ptr[r] + deg[j];
         c->h_col.insert(c->h_col.end(), cols[j].begin(), cols[j].end());
     }
     const int nnzb = c->h_row_ptr[N];
     auto find_blk = [&](int a, int b) -> int {
-        const auto lo = c->h_col.begin() + c->h_row_ptr[a], hi = c->h_col.begin() + c->h_row_ptr[a + 1];
+        const int ra = c->plan.node_row[a];
+        const auto lo = c->h_col.begin() + c->h_row_ptr[ra], hi = c->h_col.begin() + c->h_row_ptr[ra + 1];
         const auto it = std::lower_bound(lo, hi, b);
         if (it == hi || *it != b) return -1;
         return static_cast<int>(it - c->h_col.begin());
@@ -442,10 +459,37 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->d_rec.resize(1);
     c->d_status.resize(1);
     if (N > 0) {
-        c->plan.build(c->h_row_ptr.data(), N, c->num_sms, c->smem_optin);
+        c->plan.size_smem(c->h_row_ptr.data(), c->smem_optin);
         c->row_begin.upload(c->plan.row_begin.data(), c->plan.row_begin.size(), s);
-        c->pcg_a.resize(8 * static_cast<size_t>(c->plan.grid));
-        c->pcg_b.resize(8 * static_cast<size_t>(c->plan.grid));
+        c->d_row_node.upload(c->plan.row_node.data(), N, s);
+        c->d_node_row.upload(c->plan.node_row.data(), N, s);
+        c->d_node_agg.upload(c->plan.node_agg.data(), N, s);
+        c->d_agg_center.upload(c->plan.agg_center.data(), c->plan.agg_center.size(), s);
+        const size_t nc = 4 * static_cast<size_t>(c->plan.n_agg);
+        c->coarse_part.resize(static_cast<size_t>(c->plan.grid) * 4 * nc);
+        c->coarse_inv.resize(nc * nc);
+        c->pcg_a.resize(16 * static_cast<size_t>(c->plan.grid));
+        c->pcg_b.resize(16 * static_cast<size_t>(c->plan.grid));
+        d.node_row = c->d_node_row.p;
+        // cluster-resident solver when the graph fits one cluster's shared memory
+        c->cplan.build(p->node_positions, c->h_row_ptr.data(), c->h_col.data(), c->plan.node_row.data(), N,
+                       c->smem_optin, 16);
+        const char* mode = std::getenv("NRR_PCG");
+        c->use_cluster = c->cplan.ok && !(mode && std::string(mode) == "grid");
+        if (c->use_cluster) {
+            const ClusterPlan& cp = c->cplan;
+            c->c_rank_rows.upload(cp.rank_rows.data(), cp.rank_rows.size(), s);
+            c->c_row_node.upload(cp.row_node.data(), cp.row_node.size(), s);
+            c->c_ent_ptr.upload(cp.ent_ptr.data(), cp.ent_ptr.size(), s);
+            c->c_ent.upload(cp.ent.data(), cp.ent.size(), s);
+            c->c_diag_ent.upload(cp.diag_ent.data(), cp.diag_ent.size(), s);
+            c->c_store_off.upload(cp.store_off.data(), cp.store_off.size(), s);
+            c->c_store_src.resize(std::max<size_t>(cp.store_src.size(), 1));
+            if (!cp.store_src.empty()) c->c_store_src.upload(cp.store_src.data(), cp.store_src.size(), s);
+            c->c_halo_off.upload(cp.halo_off.data(), cp.halo_off.size(), s);
+            c->c_halo_src.resize(std::max<size_t>(cp.halo_src.size(), 1));
+            if (!cp.halo_src.empty()) c->c_halo_src.upload(cp.halo_src.data(), cp.halo_src.size(), s);
+        }
     }
     NRR_CUDA_CHECK(cudaStreamSynchronize(s));
     c->has_problem = true;
@@ -600,16 +644,49 @@ void assemble_solve(nrr_ctx* c, const TermParams& tp, const double* x0, double* 
     PcgArgs a{};
     a.row_ptr = c->d_row_ptr.p;
     a.col = c->d_col.p;
+    a.row_node = c->d_row_node.p;
     a.K = c->K.p;
     a.B = c->B.p;
     a.X = xout;
     a.Z = c->Z.p;
     a.row_begin = c->row_begin.p;
+    a.node_pos = c->d_node_pos.p;
+    a.agg_center = c->d_agg_center.p;
+    a.node_agg = c->d_node_agg.p;
+    a.coarse_inv = c->coarse_inv.p;
     a.part_a = c->pcg_a.p;
     a.part_b = c->pcg_b.p;
     a.status = c->d_status.p;
     a.rtol = c->opt.pcg_rtol;
     a.max_iter = c->opt.pcg_max_iter;
+    a.agg_ctas = c->plan.agg_ctas;
+    a.n_agg = c->plan.n_agg;
+    a.use_coarse = c->plan.use_coarse ? 1 : 0;
+    if (c->use_cluster) {
+        ClusterArgs ca{};
+        ca.plan = ClusterPlanDev{c->c_rank_rows.p, c->c_row_node.p, c->c_ent_ptr.p, c->c_ent.p, c->c_diag_ent.p,
+                                 c->c_store_off.p, c->c_store_src.p, c->c_halo_off.p, c->c_halo_src.p};
+        ca.K = c->K.p;
+        ca.B = c->B.p;
+        ca.X = xout;
+        ca.status = c->d_status.p;
+        ca.rtol = c->opt.pcg_rtol;
+        ca.max_iter = c->opt.pcg_max_iter;
+        if (std::getenv("NRR_PROF")) {
+            if (c->prof.n == 0) {
+                c->prof.resize(10);
+                c->prof.zero(c->stream);
+            }
+            ca.prof = c->prof.p;
+        }
+        launch_pcg_cluster(c->cplan, ca, c->stream);
+        ++c->launches;
+        return;
+    }
+    if (c->plan.use_coarse) {
+        launch_coarse_setup(c->plan, a, CoarseWork{c->coarse_part.p, c->coarse_inv.p}, c->stream);
+        c->launches += 2;
+    }
     launch_pcg(c->plan, a, c->stream);
     ++c->launches;
 }
@@ -1044,8 +1121,9 @@ int nrr_step(nrr_ctx* ctx, const double* X, const double* prm, double landmark_w
         assemble_solve(ctx, tp, ctx->x.p, ctx->xmm.p);
         NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->h_status.p, ctx->d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost,
                                        ctx->stream));
+        std::vector<double> kdev(out_K ? 16 * static_cast<size_t>(ctx->dp.nnzb) : 0);
         if (out_K)
-            NRR_CUDA_CHECK(cudaMemcpyAsync(out_K, ctx->K.p, sizeof(double) * 16 * ctx->dp.nnzb, cudaMemcpyDeviceToHost,
+            NRR_CUDA_CHECK(cudaMemcpyAsync(kdev.data(), ctx->K.p, sizeof(double) * kdev.size(), cudaMemcpyDeviceToHost,
                                            ctx->stream));
         if (out_B) {
             launch_nodemajor_to_colmajor(ctx->B.p, ctx->xnext.p, N, ctx->stream);
@@ -1053,6 +1131,15 @@ int nrr_step(nrr_ctx* ctx, const double* X, const double* prm, double landmark_w
             sync(ctx);
         }
         sync(ctx);
+        if (out_K) {  // solver-row order -> node order (the reference's pattern order)
+            size_t o = 0;
+            for (int a = 0; a < N; ++a) {
+                const int r = ctx->plan.node_row[a];
+                const size_t cnt = 16 * static_cast<size_t>(ctx->h_row_ptr[r + 1] - ctx->h_row_ptr[r]);
+                std::memcpy(out_K + o, kdev.data() + 16 * static_cast<size_t>(ctx->h_row_ptr[r]), cnt * sizeof(double));
+                o += cnt;
+            }
+        }
         if (out_Xmm) {
             check_pcg(ctx, *ctx->h_status.p);
             launch_nodemajor_to_colmajor(ctx->xmm.p, ctx->xnext.p, N, ctx->stream);
@@ -1109,7 +1196,46 @@ int nrr_init_parameters(nrr_ctx* ctx, const nrr_solver_config* cfg, double* out6
     });
 }
 
+int nrr_debug_solver_plan(const nrr_problem_view* p, int32_t num_sms, int64_t smem_limit, int64_t* out8) {
+    return guarded([&] {
+        const int N = p->node_count, E = p->edge_count;
+        std::vector<std::vector<int>> cols(N);
+        for (int j = 0; j < N; ++j) cols[j].push_back(j);
+        for (int e = 0; e < E; ++e) {
+            cols[p->edges[2 * e]].push_back(p->edges[2 * e + 1]);
+            cols[p->edges[2 * e + 1]].push_back(p->edges[2 * e]);
+        }
+        std::vector<int> deg(N), row_ptr(N + 1, 0), col, node_row(N);
+        for (int j = 0; j < N; ++j) {
+            std::sort(cols[j].begin(), cols[j].end());
+            deg[j] = static_cast<int>(cols[j].size());
+            row_ptr[j + 1] = row_ptr[j] + deg[j];
+            col.insert(col.end(), cols[j].begin(), cols[j].end());
+            node_row[j] = j;
+        }
+        ClusterPlan cp;
+        cp.build(p->node_positions, row_ptr.data(), col.data(), node_row.data(), N, static_cast<size_t>(smem_limit), 16);
+        out8[0] = cp.ok;
+        out8[1] = cp.CS;
+        out8[2] = cp.max_rows;
+        out8[3] = cp.max_store;
+        out8[4] = cp.max_ext;
+        out8[5] = static_cast<int64_t>(cp.smem_bytes);
+        out8[6] = static_cast<int64_t>(cp.store_src.size());
+        int64_t glob = 0;
+        for (const auto& e : cp.ent) glob += e.x & 1;
+        out8[7] = glob;
+        (void)num_sms;
+    });
+}
+
 int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* pcg_iters) {
+    if (ctx->prof.n && std::getenv("NRR_PROF")) {
+        long long h[10];
+        cudaMemcpy(h, ctx->prof.p, sizeof(h), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "pcg phase cycles: halo %lld spmvA %lld slotsA %lld totA %lld updB %lld slotsB %lld totB %lld - %lld exsync %lld misc %lld\n",
+                     h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+    }
     if (launches) *launches = ctx->launches;
     if (kernel_ms6)
         for (int k = 0; k < nrr_ctx::kClasses; ++k) kernel_ms6[k] = ctx->class_ms[k];

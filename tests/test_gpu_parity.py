@@ -219,7 +219,7 @@ def _energy(rep):
     return [np.array([it["E"] for it in st["iterations"]]) for st in rep["stages"]]
 
 
-def _perturbed(p, rel=1e-15):
+def _perturbed(p, rel=1e-13):
     q = R.Problem(p.source, p.target * (1.0 + rel), p.graph, p.src_avg_edge_length, p.faces)
     return q
 
@@ -263,7 +263,7 @@ def test_register_aa_parity(ctx, case):
         for k in range(n):
             if fg[k] != fo[k] or fs[k] != fo[k]:
                 break  # a revert decision flipped: the trajectories part ways
-            env = max(E_REL * abs(eo[k]), 10 * abs(es[k] - eo[k]))
+            env = E_REL * abs(eo[k]) if k < 10 else max(E_REL * abs(eo[k]), 10 * abs(es[k] - eo[k]))
             assert abs(eg[k] - eo[k]) <= env, (k, eg[k], eo[k], es[k])
         # the stage ends at the same energy level
         assert abs(eg[-1] - eo[-1]) <= max(1e-4 * abs(eo[-1]), 10 * abs(es[-1] - eo[-1]))
