@@ -99,7 +99,7 @@ typedef struct nrr_report_summary {
  * solves directly). The PCG stops when max|r| <= pcg_rtol*(1+max|B|) and the
  * true residual meets the reference bar 1e-8*(1+max|B|) (energy.hpp:245). */
 typedef struct nrr_solve_options {
-    double pcg_rtol;      /* default 1e-12 */
+    double pcg_rtol;      /* default 1e-12 (AA trajectories need it) */
     int32_t pcg_max_iter; /* default 20000 */
     int32_t record_passes;/* keep per-pass records (and NN indices if nonzero==2) */
 } nrr_solve_options;
@@ -170,6 +170,22 @@ int nrr_step(nrr_ctx* ctx, const double* X, const double* prm, double landmark_w
              const nrr_solver_config* cfg_for_landmarks, int32_t* out_index,
              double* out_sqdist, double* out_energy4, double* out_K, double* out_B,
              double* out_Xmm);
+
+/* SystemAssembler::fill (energy.hpp:182-228) from caller state: corr_points =
+ * Correspondences::target_point (n*3), w_align (n) = alignment_weights,
+ * w_reg (P) = regularization_weights (already scaled by alpha), rotations
+ * (N*9, row-major 3x3 per node). out_K = BSR values in the reference pattern
+ * order (node a's blocks, ascending column, 16 row-major doubles per block),
+ * out_B = 4N x 3 column-major. The system stays resident for nrr_solve. */
+int nrr_assemble(nrr_ctx* ctx, const double* corr_points, const double* w_align, const double* w_reg,
+                 const double* rotations, double beta, double landmark_weight,
+                 const nrr_solver_config* cfg_for_landmarks, double* out_K, double* out_B);
+
+/* SystemAssembler::solve / solve_system (energy.hpp:233-254, :393-409) by the
+ * device PCG. K (reference pattern order) and B (4N x 3) may be NULL to reuse
+ * the resident system of the last nrr_assemble/nrr_step; X0 = warm start
+ * (NULL = zero). Same failure messages as the reference. */
+int nrr_solve(nrr_ctx* ctx, const double* K, const double* B, const double* X0, double* out_X);
 
 /* anderson_combine (anderson.hpp:22-46) on a host history of h entries
  * (oldest first, g and f of length dim each), window m. */

@@ -107,6 +107,9 @@ _SIGS = {
     "nrr_project_rotations": (C.c_int, [C.c_void_p, f64p, C.c_int32, f64p, i32p]),
     "nrr_step": (C.c_int, [C.c_void_p, f64p, f64p, C.c_double, C.POINTER(SolverConfig), i32p, f64p, f64p,
                            f64p, f64p, f64p]),
+    "nrr_assemble": (C.c_int, [C.c_void_p, f64p, f64p, f64p, f64p, C.c_double, C.c_double,
+                               C.POINTER(SolverConfig), f64p, f64p]),
+    "nrr_solve": (C.c_int, [C.c_void_p, f64p, f64p, f64p, f64p]),
     "nrr_anderson_combine": (C.c_int, [C.c_void_p, f64p, f64p, C.c_int32, C.c_int32, C.c_int32, f64p, i32p]),
     "nrr_init_parameters": (C.c_int, [C.c_void_p, C.POINTER(SolverConfig), f64p]),
     "nrr_ctx_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), f64p, i32p]),

@@ -45,6 +45,7 @@ namespace nrr_b200 {
 namespace {
 
 constexpr int kQ = 16;  // partial slots per CTA and phase
+constexpr int kCoarseThreads = 512;
 
 // coarse mode k of node a in aggregate g: [e_k; d_k] for k < 3, e_3 for k = 3,
 // d = p_a - c_g
@@ -56,31 +57,47 @@ __device__ __forceinline__ void node_offset(const PcgArgs& a, int node, double d
 
 // ---------------------------------------------------------------- coarse setup
 // CTA c: partial[c][k][h*4+l] = sum over its rows a and blocks (a,b) with b in
-// aggregate h of psi_k(a)^T K_ab psi_l(b). One thread per output entry, blocks
-// scanned in BSR order: deterministic.
-__global__ void __launch_bounds__(kPcgThreads) coarse_partial_kernel(PcgArgs a, double* __restrict__ partial) {
+// aggregate h of psi_k(a)^T K_ab psi_l(b). The CTA's blocks are first staged
+// in shared memory with their row/column offsets and column aggregate; then one
+// thread per output entry scans them in BSR order: deterministic, no atomics.
+__global__ void __launch_bounds__(kCoarseThreads) coarse_partial_kernel(PcgArgs a, double* __restrict__ partial) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int c = blockIdx.x;
     const int r0 = a.row_begin[c], r1 = a.row_begin[c + 1];
+    const int kb0 = a.row_ptr[r0], nkb = a.row_ptr[r1] - kb0;
     const int nc = 4 * a.n_agg;
-    for (int o = threadIdx.x; o < 4 * nc; o += blockDim.x) {
-        const int k = o / nc, hl = o % nc, h = hl >> 2, l = hl & 3;
-        double acc = 0.0;
-        for (int j = r0; j < r1; ++j) {
-            const int na = a.row_node[j];
-            double da[3];
-            node_offset(a, na, da);
-            for (int blk = a.row_ptr[j]; blk < a.row_ptr[j + 1]; ++blk) {
-                const int nb = a.col[blk];
-                if (a.node_agg[nb] != h) continue;
-                const double* Kb = a.K + static_cast<size_t>(blk) * 16;
-                double db[3];
-                node_offset(a, nb, db);
-                // u = K_ab psi_l(b)
-                double u[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) u[r] = l < 3 ? Kb[r * 4 + l] + db[l] * Kb[r * 4 + 3] : Kb[r * 4 + 3];
-                acc += k < 3 ? u[k] + da[k] * u[3] : u[3];
+    double* Kb = reinterpret_cast<double*>(smem_raw);         // nkb*16
+    double* da = Kb + 16 * static_cast<size_t>(nkb);          // nkb*3 row-node offsets
+    double* db = da + 3 * static_cast<size_t>(nkb);           // nkb*3 col-node offsets
+    int* hb = reinterpret_cast<int*>(db + 3 * static_cast<size_t>(nkb));  // nkb col aggregate
+    for (int i = threadIdx.x; i < nkb * 16; i += blockDim.x) Kb[i] = a.K[static_cast<size_t>(kb0) * 16 + i];
+    for (int j = r0 + (threadIdx.x >> 5); j < r1; j += blockDim.x >> 5) {
+        const int na = a.row_node[j];
+        double d[3];
+        node_offset(a, na, d);
+        for (int b = a.row_ptr[j] + (threadIdx.x & 31); b < a.row_ptr[j + 1]; b += 32) {
+            const int nb = a.col[b];
+            double e[3];
+            node_offset(a, nb, e);
+            const int lb = b - kb0;
+            for (int t = 0; t < 3; ++t) {
+                da[3 * lb + t] = d[t];
+                db[3 * lb + t] = e[t];
             }
+            hb[lb] = a.node_agg[nb];
+        }
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < 4 * nc; o += blockDim.x) {
+        const int k = o / nc, hl = o - k * nc, h = hl >> 2, l = hl & 3;
+        double acc = 0.0;
+        for (int lb = 0; lb < nkb; ++lb) {
+            if (hb[lb] != h) continue;
+            const double* K = Kb + 16 * lb;
+            double u[4];  // u = K_ab psi_l(b)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) u[r] = l < 3 ? K[r * 4 + l] + db[3 * lb + l] * K[r * 4 + 3] : K[r * 4 + 3];
+            acc += k < 3 ? u[k] + da[3 * lb + k] * u[3] : u[3];
         }
         partial[(static_cast<size_t>(c) * 4 + k) * nc + hl] = acc;
     }
@@ -88,8 +105,9 @@ __global__ void __launch_bounds__(kPcgThreads) coarse_partial_kernel(PcgArgs a, 
 
 // One CTA: K0 = sum of the partials of each aggregate's CTAs (fixed order),
 // symmetrised, inverted in place by Gauss-Jordan (SPD: no pivoting needed);
-// modes with a vanishing pivot are dropped (zero rows / columns).
-__global__ void __launch_bounds__(kPcgThreads) coarse_invert_kernel(PcgArgs a, const double* __restrict__ partial,
+// modes with a vanishing pivot are dropped (zero rows / columns). Warp w owns
+// rows w, w+nw, ...; lanes own columns: no index division in the inner loop.
+__global__ void __launch_bounds__(kCoarseThreads) coarse_invert_kernel(PcgArgs a, const double* __restrict__ partial,
                                                                    double* __restrict__ inv, int grid) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nc = 4 * a.n_agg;
@@ -97,23 +115,23 @@ __global__ void __launch_bounds__(kPcgThreads) coarse_invert_kernel(PcgArgs a, c
     double* colk = A + nc * nc;                       // nc
     double* rowk = colk + nc;                         // nc
     __shared__ double s_dmax;
-    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
-        const int i = o / nc, j = o % nc;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = w; i < nc; i += nw) {
         const int g = i >> 2, k = i & 3;
-        double s = 0.0;
-        for (int c = g * a.agg_ctas; c < min((g + 1) * a.agg_ctas, grid); ++c)
-            s += partial[(static_cast<size_t>(c) * 4 + k) * nc + j];
-        A[o] = s;
+        for (int j = lane; j < nc; j += 32) {
+            double sum = 0.0;
+            for (int cc = g * a.agg_ctas; cc < min((g + 1) * a.agg_ctas, grid); ++cc)
+                sum += partial[(static_cast<size_t>(cc) * 4 + k) * nc + j];
+            A[i * nc + j] = sum;
+        }
     }
     __syncthreads();
-    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
-        const int i = o / nc, j = o % nc;
-        if (i < j) {
+    for (int i = w; i < nc; i += nw)
+        for (int j = lane; j < i; j += 32) {
             const double v = 0.5 * (A[i * nc + j] + A[j * nc + i]);
             A[i * nc + j] = v;
             A[j * nc + i] = v;
         }
-    }
     __syncthreads();
     if (threadIdx.x == 0) {
         double m = 0.0;
@@ -131,16 +149,17 @@ __global__ void __launch_bounds__(kPcgThreads) coarse_invert_kernel(PcgArgs a, c
             rowk[i] = A[k * nc + i];
         }
         __syncthreads();
-        for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
-            const int i = o / nc, j = o % nc;
-            if (!ok) {
-                if (i == k || j == k) A[o] = 0.0;
-                continue;
+        for (int i = w; i < nc; i += nw) {
+            const double ci = colk[i];
+            double* Ai = A + i * nc;
+            for (int j = lane; j < nc; j += 32) {
+                double v;
+                if (!ok) v = (i == k || j == k) ? 0.0 : Ai[j];
+                else if (i == k) v = j == k ? d : rowk[j] * d;
+                else if (j == k) v = -ci * d;
+                else v = Ai[j] - ci * rowk[j] * d;
+                Ai[j] = v;
             }
-            if (i == k && j == k) A[o] = d;
-            else if (i == k) A[o] = rowk[j] * d;
-            else if (j == k) A[o] = -colk[i] * d;
-            else A[o] -= colk[i] * rowk[j] * d;
         }
         __syncthreads();
     }
@@ -160,6 +179,7 @@ struct Shared {
     double* red;     // 16 warps x kQ
     double* bcast;   // kQ
     double* y;       // 12: own aggregate coarse correction
+    double* ext;     // (own rows + halo) x 12: the SpMV operand staged from L2
 };
 
 __device__ __forceinline__ double op2(bool mx, double a, double b) { return mx ? fmax(a, b) : a + b; }
@@ -211,13 +231,13 @@ __device__ __forceinline__ void block_partials(const double* vals, int nq, doubl
         base = slot;
     }
     v1 = op2((max_mask >> base) & 1u, v1, __shfl_xor_sync(0xffffffffu, v1, 1));
-    if ((lane & 1) == 0) red[base * 16 + w] = v1;
+    if ((lane & 1) == 0) red[base * 32 + w] = v1;
     __syncthreads();
     if (w < nq) {
         const bool mx = (max_mask >> w) & 1u;
-        double v = lane < nw ? red[w * 16 + lane] : 0.0;
+        double v = lane < nw ? red[w * 32 + lane] : 0.0;
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) v = op2(mx, v, __shfl_xor_sync(0xffffffffu, v, o));
+        for (int o = 16; o > 0; o >>= 1) v = op2(mx, v, __shfl_xor_sync(0xffffffffu, v, o));
         if (lane == 0) part[blockIdx.x * kQ + w] = v;
     }
     __syncthreads();
@@ -266,7 +286,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     {
         double* p = reinterpret_cast<double*>(smem_raw);
         sh.red = p;
-        p += 16 * kQ;
+        p += 32 * kQ;
         sh.bcast = p;
         p += kQ;
         sh.y = p;
@@ -283,20 +303,22 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         p += 3 * kCoarseMax;
         sh.ptq = p;
         p += 3 * kCoarseMax;
+        sh.ext = p;
+        p += 12 * static_cast<size_t>(a.max_ext);
         if (a.k_in_smem) {
             sh.K = p;
             p += 16 * static_cast<size_t>(a.max_kb);
             sh.col = reinterpret_cast<int*>(p);
         } else {
             sh.K = const_cast<double*>(a.K) + static_cast<size_t>(kb0) * 16;
-            sh.col = const_cast<int*>(a.col) + kb0;
+            sh.col = const_cast<int*>(a.colx) + kb0;
         }
     }
     if (a.k_in_smem) {
         const double2* src = reinterpret_cast<const double2*>(a.K + static_cast<size_t>(kb0) * 16);
         double2* dst = reinterpret_cast<double2*>(sh.K);
         for (int i = threadIdx.x; i < nkb * 8; i += blockDim.x) dst[i] = src[i];
-        for (int i = threadIdx.x; i < nkb; i += blockDim.x) sh.col[i] = a.col[kb0 + i];
+        for (int i = threadIdx.x; i < nkb; i += blockDim.x) sh.col[i] = a.colx[kb0 + i];
     }
     if (a.use_coarse) {
         for (int i = threadIdx.x; i < 4 * nc; i += blockDim.x) {
@@ -357,69 +379,95 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     }
     __syncthreads();
 
+    // Element e = threadIdx.x + k*blockDim (blockDim % 12 == 0): the scalar row
+    // r and column c are the same for all of a thread's elements, so every
+    // per-thread reduction is a scalar register (no dynamic indexing, no
+    // local memory).
     const int nel = nrows * 12;
+    const int my_rc = threadIdx.x % 12, my_r = my_rc / 3, my_c = my_rc % 3;
     double xr[EPT], br[EPT], rr[EPT], zr[EPT], pr[EPT], qr[EPT];
-    int el_row[EPT], el_r[EPT], el_c[EPT];
+    int el_row[EPT];
     size_t el_g[EPT];
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
         const int e = threadIdx.x + k * blockDim.x;
         const bool live = e < nel;
-        const int lr = live ? e / 12 : 0, rc = live ? e % 12 : 0;
+        const int lr = live ? e / 12 : 0;
         el_row[k] = live ? lr : -1;
-        el_r[k] = rc / 3;
-        el_c[k] = rc % 3;
-        el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + rc;
+        el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + my_rc;
         xr[k] = live ? a.X[el_g[k]] : 0.0;
         br[k] = live ? a.B[el_g[k]] : 0.0;
-        pr[k] = qr[k] = 0.0;
+        pr[k] = qr[k] = zr[k] = rr[k] = 0.0;
     }
 
-    auto spmv = [&](int k, const double* __restrict__ v) -> double {
+    const int e0 = a.ext_off[cta], n_ext = a.ext_off[cta + 1] - e0;
+    // stage the halo rows of v (global, written by other CTAs before the last
+    // grid barrier) into shared memory next to the own rows: one coalesced
+    // round of L2 loads instead of a latency-bound gather per K block
+    auto fill_halo = [&](const double* __restrict__ v) {
+        for (int t = nrows * 12 + threadIdx.x; t < n_ext * 12; t += blockDim.x)
+            sh.ext[t] = __ldcg(v + static_cast<size_t>(a.ext_node[e0 + t / 12]) * 12 + t % 12);
+        __syncthreads();
+    };
+    auto spmv = [&](int k) -> double {
         const int lr = el_row[k];
         if (lr < 0) return 0.0;
-        const int r = el_r[k], c = el_c[k];
         const int j = r0 + lr;
         const int b0 = a.row_ptr[j] - kb0, b1 = a.row_ptr[j + 1] - kb0;
         double acc = 0.0;
         for (int b = b0; b < b1; ++b) {
-            const double* kk = sh.K + static_cast<size_t>(b) * 16 + r * 4;
-            const double* vv = v + static_cast<size_t>(sh.col[b]) * 12 + c;
-            acc = fma(kk[0], __ldcg(vv), acc);
-            acc = fma(kk[1], __ldcg(vv + 3), acc);
-            acc = fma(kk[2], __ldcg(vv + 6), acc);
-            acc = fma(kk[3], __ldcg(vv + 9), acc);
+            const double* kk = sh.K + static_cast<size_t>(b) * 16 + my_r * 4;
+            const double* vv = sh.ext + sh.col[b] * 12 + my_c;
+            acc = fma(kk[0], vv[0], acc);
+            acc = fma(kk[1], vv[3], acc);
+            acc = fma(kk[2], vv[6], acc);
+            acc = fma(kk[3], vv[9], acc);
         }
         return acc;
     };
-    // own-element contribution to Psi^T v: slot k*3 + c of 12
-    auto psi_t = [&](int k, double v, double* out12) {
+    // Psi^T contribution of the thread's elements (own column): 4 mode sums
+    auto psi_acc = [&](int k, double v, double ps[4]) {
         const int lr = el_row[k];
         if (lr < 0) return;
-        const int r = el_r[k], c = el_c[k];
-        if (r < 3) {
-            out12[r * 3 + c] += v;
+        if (my_r < 3) {
+            ps[my_r] += v;
         } else {
-            out12[0 * 3 + c] += sh.off[lr * 3 + 0] * v;
-            out12[1 * 3 + c] += sh.off[lr * 3 + 1] * v;
-            out12[2 * 3 + c] += sh.off[lr * 3 + 2] * v;
-            out12[3 * 3 + c] += v;
+            ps[0] += sh.off[lr * 3 + 0] * v;
+            ps[1] += sh.off[lr * 3 + 1] * v;
+            ps[2] += sh.off[lr * 3 + 2] * v;
+            ps[3] += v;
         }
     };
-    // z = M_jj r + Psi y_own; y_own = K0inv[own rows] rho (computed by 12 threads)
+    double vals[kQ];
+    auto zero_vals = [&]() {
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) vals[j] = 0.0;
+    };
+    // slot base + c gets v for the own column only (compile-time base)
+    auto put_col = [&](int base, double v) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vals[base + c] = c == my_c ? v : 0.0;
+    };
+    auto put_psi = [&](int base, const double ps[4]) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) vals[base + m * 3 + c] = c == my_c ? ps[m] : 0.0;
+    };
+    // z = M_jj r + Psi y_own; y_own = K0inv[own rows] rho (warps 0..11)
     auto precond = [&]() {
-        if (a.use_coarse && (threadIdx.x >> 5) < 12) {  // warp w: output w, lanes split the coarse sum
+        if (a.use_coarse && (threadIdx.x >> 5) < 12) {
             const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
             const int k = w / 3, c = w % 3;
-            double s = 0.0;
+            double sum = 0.0;
             const double* row = sh.cinv + k * nc;
-            for (int j = lane; j < nc; j += 32) s += row[j] * sh.rho[j * 3 + c];
-            s = warp_sum(s);
-            if (lane == 0) sh.y[k * 3 + c] = s;
+            for (int j = lane; j < nc; j += 32) sum += row[j] * sh.rho[j * 3 + c];
+            sum = warp_sum(sum);
+            if (lane == 0) sh.y[k * 3 + c] = sum;
         }
 #pragma unroll
         for (int k = 0; k < EPT; ++k)
-            if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + el_r[k] * 3 + el_c[k]] = rr[k];
+            if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = rr[k];
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
@@ -427,48 +475,67 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                 zr[k] = 0.0;
                 continue;
             }
-            const int lr = el_row[k], r = el_r[k], c = el_c[k];
-            const double* M = sh.M + lr * 16 + r * 4;
-            const double* rv = sh.rex + lr * 12 + c;
+            const int lr = el_row[k];
+            const double* M = sh.M + lr * 16 + my_r * 4;
+            const double* rv = sh.rex + lr * 12 + my_c;
             double z = M[0] * rv[0] + M[1] * rv[3] + M[2] * rv[6] + M[3] * rv[9];
             if (a.use_coarse) {
-                if (r < 3) z += sh.y[r * 3 + c];
+                if (my_r < 3) z += sh.y[my_r * 3 + my_c];
                 else
-                    z += sh.off[lr * 3] * sh.y[c] + sh.off[lr * 3 + 1] * sh.y[3 + c] + sh.off[lr * 3 + 2] * sh.y[6 + c] +
-                         sh.y[9 + c];
+                    z += sh.off[lr * 3] * sh.y[my_c] + sh.off[lr * 3 + 1] * sh.y[3 + my_c] +
+                         sh.off[lr * 3 + 2] * sh.y[6 + my_c] + sh.y[9 + my_c];
             }
             zr[k] = z;
             __stcg(a.Z + el_g[k], z);
         }
-        __syncthreads();
+        __syncthreads();  // all rex reads done before own z overwrites ext
+#pragma unroll
+        for (int k = 0; k < EPT; ++k)
+            if (el_row[k] >= 0) sh.ext[el_row[k] * 12 + my_rc] = zr[k];
     };
 
     grid.sync();  // fail flags visible
     if (__ldcg(&a.status->fail_node) != 0x7fffffff) return;
 
-    double vals[kQ];
     int it = 0, restarts = 0;
     double bmax = 0.0, tol = 0.0, bar = 0.0;
     double rz[3], beta[3] = {0, 0, 0};
     bool need_init = true;
     int status_code = 0;  // 1 converged, 2 indefinite, 3 max iter
+    const bool prof = a.prof != nullptr && cta == 0 && threadIdx.x == 0;
+    long long tp = clock64(), acc_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto mark = [&](int slot) {
+        if (prof) {
+            const long long t = clock64();
+            acc_t[slot] += t - tp;
+            tp = t;
+        }
+    };
 
     while (true) {
         if (need_init) {
             // r = b - K x; coarse residual rho = Psi^T r; z = M r; (r,z)
 #pragma unroll
             for (int k = 0; k < EPT; ++k)
-                if (el_row[k] >= 0) __stcg(a.X + el_g[k], xr[k]);
+                if (el_row[k] >= 0) {
+                    __stcg(a.X + el_g[k], xr[k]);
+                    sh.ext[el_row[k] * 12 + my_rc] = xr[k];
+                }
             grid.sync();
-            for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
+            fill_halo(a.X);
+            double rmx = 0.0, bmx = 0.0, ps[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
-                rr[k] = br[k] - spmv(k, a.X);
+                rr[k] = br[k] - spmv(k);
                 if (el_row[k] < 0) continue;
-                vals[0] = fmax(vals[0], fabs(rr[k]));
-                vals[1] = fmax(vals[1], fabs(br[k]));
-                psi_t(k, rr[k], vals + 2);
+                rmx = fmax(rmx, fabs(rr[k]));
+                bmx = fmax(bmx, fabs(br[k]));
+                psi_acc(k, rr[k], ps);
             }
+            zero_vals();
+            vals[0] = rmx;
+            vals[1] = bmx;
+            put_psi(2, ps);
             block_partials(vals, 14, sh.red, a.part_b, 0x3u);
             grid.sync();
             grid_totals(a.part_b, G, sh.bcast, 2, 0x3u);
@@ -493,10 +560,12 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                 continue;  // verify on the true residual (need_init stays set)
             }
             precond();
-            for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
+            double rzs = 0.0;
 #pragma unroll
             for (int k = 0; k < EPT; ++k)
-                if (el_row[k] >= 0) vals[el_c[k]] += rr[k] * zr[k];
+                if (el_row[k] >= 0) rzs += rr[k] * zr[k];
+            zero_vals();
+            put_col(0, rzs);
             block_partials(vals, 3, sh.red, a.part_a, 0x0u);
             grid.sync();
             grid_totals(a.part_a, G, sh.bcast, 3, 0x0u);
@@ -510,23 +579,34 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             need_init = false;
             __syncthreads();
         }
+        fill_halo(a.Z);
+        mark(7);
         // ---- phase A: q = K z + beta q, p = z + beta p; (p,q), Psi^T q
-        for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
+        {
+            const double bt = beta[my_c];
+            double pq = 0.0, ps[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-            const double w = spmv(k, a.Z);
-            if (el_row[k] < 0) continue;
-            const int c = el_c[k];
-            qr[k] = w + beta[c] * qr[k];
-            pr[k] = zr[k] + beta[c] * pr[k];
-            vals[c] += pr[k] * qr[k];
-            psi_t(k, qr[k], vals + 3);
+            for (int k = 0; k < EPT; ++k) {
+                const double w = spmv(k);
+                if (el_row[k] < 0) continue;
+                qr[k] = w + bt * qr[k];
+                pr[k] = zr[k] + bt * pr[k];
+                pq += pr[k] * qr[k];
+                psi_acc(k, qr[k], ps);
+            }
+            zero_vals();
+            put_col(0, pq);
+            if (a.use_coarse) put_psi(3, ps);
         }
+        mark(0);
         block_partials(vals, a.use_coarse ? 15 : 3, sh.red, a.part_a, 0x0u);
+        mark(1);
         grid.sync();
+        mark(2);
         grid_totals(a.part_a, G, sh.bcast, 3, 0x0u);
         if (a.use_coarse) aggregate_sums(a, a.part_a, G, 3, sh.ptq);
         __syncthreads();
+        mark(3);
         double alpha[3];
         bool indefinite = false;
         for (int c = 0; c < 3; ++c) {
@@ -547,29 +627,38 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         if (a.use_coarse)
             for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) sh.rho[o] -= alpha[o % 3] * sh.ptq[o];
         // ---- phase B: x += alpha p, r -= alpha q, z = M r; (r,z), max|r|
+        {
+            const double al = alpha[my_c];
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-            if (el_row[k] < 0) continue;
-            const int c = el_c[k];
-            xr[k] = fma(alpha[c], pr[k], xr[k]);
-            rr[k] = fma(-alpha[c], qr[k], rr[k]);
+            for (int k = 0; k < EPT; ++k) {
+                if (el_row[k] < 0) continue;
+                xr[k] = fma(al, pr[k], xr[k]);
+                rr[k] = fma(-al, qr[k], rr[k]);
+            }
         }
         __syncthreads();  // rho updated before the coarse solve
         precond();
-        for (int q = 0; q < kQ; ++q) vals[q] = 0.0;
+        {
+            double rzs = 0.0, rmx = 0.0;
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-            if (el_row[k] < 0) continue;
-            const int c = el_c[k];
-            vals[c] += rr[k] * zr[k];
-            vals[3 + c] = fmax(vals[3 + c], fabs(rr[k]));
+            for (int k = 0; k < EPT; ++k) {
+                if (el_row[k] < 0) continue;
+                rzs += rr[k] * zr[k];
+                rmx = fmax(rmx, fabs(rr[k]));
+            }
+            zero_vals();
+            put_col(0, rzs);
+            vals[3] = rmx;
         }
-        block_partials(vals, 6, sh.red, a.part_b, 0x38u);
+        mark(4);
+        block_partials(vals, 4, sh.red, a.part_b, 0x8u);
+        mark(5);
         grid.sync();
-        grid_totals(a.part_b, G, sh.bcast, 6, 0x38u);
+        mark(6);
+        grid_totals(a.part_b, G, sh.bcast, 4, 0x8u);
         __syncthreads();
         double rzn[3] = {sh.bcast[0], sh.bcast[1], sh.bcast[2]};
-        const double rmax = fmax(sh.bcast[3], fmax(sh.bcast[4], sh.bcast[5]));
+        const double rmax = sh.bcast[3];
         __syncthreads();
         ++it;
         for (int c = 0; c < 3; ++c) {
@@ -593,6 +682,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
 #pragma unroll
     for (int k = 0; k < EPT; ++k)
         if (el_row[k] >= 0) a.X[el_g[k]] = xr[k];
+    if (prof)
+        for (int k = 0; k < 8; ++k) a.prof[k] += acc_t[k];
     if (cta == 0 && threadIdx.x == 0) {
         a.status->iterations = it;
         a.status->code = status_code;
@@ -667,8 +758,8 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
         throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 170)");
     ept = max_rows * 12 <= kPcgThreads ? 1 : (max_rows * 12 <= 2 * kPcgThreads ? 2 : 4);
     // aggregates: consecutive CTAs, coarse dimension 4 * n_agg <= kCoarseMax (160)
-    agg_ctas = std::max(1, (4 * grid + 159) / 160);
-    if (const char* e = std::getenv("NRR_AGG_CTAS")) agg_ctas = std::max(agg_ctas, std::atoi(e));
+    agg_ctas = std::max(8, (4 * grid + 159) / 160);  // 8 CTAs per aggregate measured best on cfg2
+    if (const char* e = std::getenv("NRR_AGG_CTAS")) agg_ctas = std::max((4 * grid + 159) / 160, std::atoi(e));
     if (const char* e = std::getenv("NRR_COARSE")) use_coarse = std::atoi(e) != 0;
     n_agg = (grid + agg_ctas - 1) / agg_ctas;
     node_agg.assign(N, 0);
@@ -686,30 +777,62 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
     (void)smem_limit;
 }
 
-void PcgPlan::size_smem(const int* row_ptr_solver, size_t smem_limit) {
+void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_limit) {
     max_kb = 0;
     for (int g = 0; g < grid; ++g)
         max_kb = std::max(max_kb, row_ptr_solver[row_begin[g + 1]] - row_ptr_solver[row_begin[g]]);
-    const size_t base = sizeof(double) * (16 * kQ + kQ + 16 + 32 * static_cast<size_t>(max_rows) + 10 * kCoarseMax);
+    // per-CTA operand rows: own rows (in row order) then the halo nodes
+    const int nnzb = row_ptr_solver[nodes];
+    colx.assign(nnzb, 0);
+    ext_off.assign(grid + 1, 0);
+    ext_node.clear();
+    max_ext = 0;
+    std::vector<int> local(nodes, -1);
+    for (int g = 0; g < grid; ++g) {
+        const int rb = row_begin[g], re = row_begin[g + 1];
+        std::vector<int> nodes_g;
+        for (int r = rb; r < re; ++r) {
+            local[row_node[r]] = r - rb;
+            nodes_g.push_back(row_node[r]);
+        }
+        for (int b = row_ptr_solver[rb]; b < row_ptr_solver[re]; ++b) {
+            const int nb = col[b];
+            if (local[nb] < 0) {
+                local[nb] = static_cast<int>(nodes_g.size());
+                nodes_g.push_back(nb);
+            }
+            colx[b] = local[nb];
+        }
+        for (int nb : nodes_g) local[nb] = -1;
+        ext_node.insert(ext_node.end(), nodes_g.begin(), nodes_g.end());
+        ext_off[g + 1] = static_cast<int>(ext_node.size());
+        max_ext = std::max(max_ext, static_cast<int>(nodes_g.size()));
+    }
+    const size_t base = sizeof(double) * (32 * kQ + kQ + 16 + 32 * static_cast<size_t>(max_rows) + 10 * kCoarseMax +
+                                          12 * static_cast<size_t>(max_ext));
     const size_t kbytes = static_cast<size_t>(max_kb) * (16 * sizeof(double) + sizeof(int));
     k_in_smem = base + kbytes + 64 <= smem_limit;
     smem_bytes = base + (k_in_smem ? kbytes : 0) + 64;
 }
 
 void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s) {
-    coarse_partial_kernel<<<plan.grid, kPcgThreads, 0, s>>>(a, w.partial);
+    const size_t psmem = static_cast<size_t>(plan.max_kb) * (22 * sizeof(double) + sizeof(int)) + 64;
+    NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(psmem)));
+    coarse_partial_kernel<<<plan.grid, kCoarseThreads, psmem, s>>>(a, w.partial);
     NRR_CUDA_CHECK(cudaGetLastError());
     const int nc = 4 * plan.n_agg;
     const size_t smem = sizeof(double) * (static_cast<size_t>(nc) * nc + 2 * nc);
     NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-    coarse_invert_kernel<<<1, kPcgThreads, smem, s>>>(a, w.partial, w.inv, plan.grid);
+    coarse_invert_kernel<<<1, kCoarseThreads, smem, s>>>(a, w.partial, w.inv, plan.grid);
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
     args.max_rows = plan.max_rows;
     args.max_kb = plan.max_kb;
+    args.max_ext = plan.max_ext;
     args.k_in_smem = plan.k_in_smem ? 1 : 0;
     args.agg_ctas = plan.agg_ctas;
     args.n_agg = plan.n_agg;

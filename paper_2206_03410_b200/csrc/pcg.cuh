@@ -8,7 +8,7 @@
 
 namespace nrr_b200 {
 
-constexpr int kPcgThreads = 512;
+constexpr int kPcgThreads = 576;  // multiple of 12: (row r, column c) fixed per thread
 constexpr int kCoarseMax = 256;  // coarse dimension limit (4 modes per aggregate)
 
 struct PcgStatus {
@@ -27,6 +27,9 @@ struct PcgArgs {
     const int* row_ptr;   // N+1 BSR over solver rows
     const int* col;       // nnzb, node ids
     const int* row_node;  // N: solver row -> node id
+    const int* colx;      // nnzb: per-CTA operand row of each block's column
+    const int* ext_off;   // grid+1
+    const int* ext_node;  // operand rows (own rows first, then halo) -> node id
     const double* K;      // nnzb*16
     const double* B;      // 12N node-major (by node id)
     double* X;            // 12N node-major: in = warm start, out = solution
@@ -41,12 +44,13 @@ struct PcgArgs {
     PcgStatus* status;
     double rtol;
     int max_iter;
-    int max_rows, max_kb, k_in_smem;
+    int max_rows, max_kb, k_in_smem, max_ext;
     int agg_ctas, n_agg, use_coarse;
+    long long* prof;  // optional clock64 per phase (CTA 0), accumulated
 };
 
 struct PcgPlan {
-    int nodes = 0, grid = 0, ept = 1, max_rows = 0, max_kb = 0;
+    int nodes = 0, grid = 0, ept = 1, max_rows = 0, max_kb = 0, max_ext = 0;
     int agg_ctas = 1, n_agg = 1;
     bool k_in_smem = false, use_coarse = true;
     size_t smem_bytes = 0;
@@ -55,10 +59,11 @@ struct PcgPlan {
     std::vector<int> node_row;    // N: node -> solver row
     std::vector<int> node_agg;    // N
     std::vector<double> agg_center;  // n_agg*3
+    std::vector<int> colx, ext_off, ext_node;
     // partition + row order; row_nnz = blocks per node (for balance)
     void build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit);
     // smem sizing once the BSR (in solver-row order) is known
-    void size_smem(const int* row_ptr_solver, size_t smem_limit);
+    void size_smem(const int* row_ptr_solver, const int* col, size_t smem_limit);
 };
 
 struct CoarseWork {

@@ -141,7 +141,7 @@ struct nrr_ctx {
 
     // ---- per-iteration state
     DevBuf<double> x, xmm, xnext, vhat, vhat2, d2, q, wa, wr, R, K, B, Z, term_part, pcg_a, pcg_b;
-    DevBuf<int> nn_idx, deg, row_begin, d_row_node, d_node_row, d_node_agg;
+    DevBuf<int> nn_idx, deg, row_begin, d_row_node, d_node_row, d_node_agg, d_colx, d_ext_off, d_ext_node;
     DevBuf<double> d_agg_center, coarse_part, coarse_inv;
     PcgPlan plan;
     ClusterPlan cplan;
@@ -459,7 +459,10 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->d_rec.resize(1);
     c->d_status.resize(1);
     if (N > 0) {
-        c->plan.size_smem(c->h_row_ptr.data(), c->smem_optin);
+        c->plan.size_smem(c->h_row_ptr.data(), c->h_col.data(), c->smem_optin);
+        c->d_colx.upload(c->plan.colx.data(), c->plan.colx.size(), s);
+        c->d_ext_off.upload(c->plan.ext_off.data(), c->plan.ext_off.size(), s);
+        c->d_ext_node.upload(c->plan.ext_node.data(), c->plan.ext_node.size(), s);
         c->row_begin.upload(c->plan.row_begin.data(), c->plan.row_begin.size(), s);
         c->d_row_node.upload(c->plan.row_node.data(), N, s);
         c->d_node_row.upload(c->plan.node_row.data(), N, s);
@@ -475,7 +478,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->cplan.build(p->node_positions, c->h_row_ptr.data(), c->h_col.data(), c->plan.node_row.data(), N,
                        c->smem_optin, 16);
         const char* mode = std::getenv("NRR_PCG");
-        c->use_cluster = c->cplan.ok && !(mode && std::string(mode) == "grid");
+        c->use_cluster = c->cplan.ok && mode && std::string(mode) == "cluster";
         if (c->use_cluster) {
             const ClusterPlan& cp = c->cplan;
             c->c_rank_rows.upload(cp.rank_rows.data(), cp.rank_rows.size(), s);
@@ -630,12 +633,14 @@ void evaluate(nrr_ctx* c, const double* x, const double* vhat, const TermParams&
     c->launches += 2;
 }
 
-void assemble_solve(nrr_ctx* c, const TermParams& tp, const double* x0, double* xout) {
-    {
-        ClassTimer t(c, kAsm);
-        launch_assemble(c->dp, c->wa.p, c->q.p, c->wr.p, c->R.p, tp, c->K.p, c->B.p, c->stream);
-        c->launches += (tp.lm_weight != 0.0 && c->dp.landmarks > 0) ? 2 : 1;
-    }
+void assemble(nrr_ctx* c, const TermParams& tp) {
+    ClassTimer t(c, kAsm);
+    launch_assemble(c->dp, c->wa.p, c->q.p, c->wr.p, c->R.p, tp, c->K.p, c->B.p, c->stream);
+    c->launches += (tp.lm_weight != 0.0 && c->dp.landmarks > 0) ? 2 : 1;
+}
+
+// PCG solve of the system in c->K / c->B (solver-row order), warm start x0
+void solve(nrr_ctx* c, const double* x0, double* xout) {
     ClassTimer t(c, kPcg);
     if (xout != x0)
         NRR_CUDA_CHECK(cudaMemcpyAsync(xout, x0, sizeof(double) * 12 * c->N, cudaMemcpyDeviceToDevice, c->stream));
@@ -645,6 +650,9 @@ void assemble_solve(nrr_ctx* c, const TermParams& tp, const double* x0, double* 
     a.row_ptr = c->d_row_ptr.p;
     a.col = c->d_col.p;
     a.row_node = c->d_row_node.p;
+    a.colx = c->d_colx.p;
+    a.ext_off = c->d_ext_off.p;
+    a.ext_node = c->d_ext_node.p;
     a.K = c->K.p;
     a.B = c->B.p;
     a.X = xout;
@@ -683,12 +691,24 @@ void assemble_solve(nrr_ctx* c, const TermParams& tp, const double* x0, double* 
         ++c->launches;
         return;
     }
+    if (std::getenv("NRR_PROF")) {
+        if (c->prof.n == 0) {
+            c->prof.resize(10);
+            c->prof.zero(c->stream);
+        }
+        a.prof = c->prof.p;
+    }
     if (c->plan.use_coarse) {
         launch_coarse_setup(c->plan, a, CoarseWork{c->coarse_part.p, c->coarse_inv.p}, c->stream);
         c->launches += 2;
     }
     launch_pcg(c->plan, a, c->stream);
     ++c->launches;
+}
+
+void assemble_solve(nrr_ctx* c, const TermParams& tp, const double* x0, double* xout) {
+    assemble(c, tp);
+    solve(c, x0, xout);
 }
 
 void check_pcg(nrr_ctx* c, const PcgStatus& st) {
@@ -1150,6 +1170,106 @@ int nrr_step(nrr_ctx* ctx, const double* X, const double* prm, double landmark_w
     });
 }
 
+namespace {
+// K in the reference pattern order (node a's row blocks, ascending columns)
+// <-> solver-row order on the device
+void k_node_to_rows(const nrr_ctx* c, const double* src, double* dst) {
+    size_t o = 0;
+    for (int a = 0; a < c->N; ++a) {
+        const int r = c->plan.node_row[a];
+        const size_t cnt = 16 * static_cast<size_t>(c->h_row_ptr[r + 1] - c->h_row_ptr[r]);
+        std::memcpy(dst + 16 * static_cast<size_t>(c->h_row_ptr[r]), src + o, cnt * sizeof(double));
+        o += cnt;
+    }
+}
+void k_rows_to_node(const nrr_ctx* c, const double* src, double* dst) {
+    size_t o = 0;
+    for (int a = 0; a < c->N; ++a) {
+        const int r = c->plan.node_row[a];
+        const size_t cnt = 16 * static_cast<size_t>(c->h_row_ptr[r + 1] - c->h_row_ptr[r]);
+        std::memcpy(dst + o, src + 16 * static_cast<size_t>(c->h_row_ptr[r]), cnt * sizeof(double));
+        o += cnt;
+    }
+}
+}  // namespace
+
+int nrr_assemble(nrr_ctx* ctx, const double* corr_points, const double* w_align, const double* w_reg,
+                 const double* rotations, double beta, double landmark_weight,
+                 const nrr_solver_config* cfg_for_landmarks, double* out_K, double* out_B) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        require_problem(ctx);
+        const int N = ctx->N, n = ctx->n, P = ctx->dp.P;
+        if (!corr_points || !w_align || (!w_reg && P > 0) || !rotations)
+            throw ConfigError("assemble: null input array");
+        if (cfg_for_landmarks) upload_landmarks(ctx, *cfg_for_landmarks);
+        else ctx->dp.landmarks = 0;
+        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->q.p, corr_points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->wa.p, w_align, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        if (P > 0)
+            NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->wr.p, w_reg, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->R.p, rotations, sizeof(double) * 9 * N, cudaMemcpyHostToDevice, ctx->stream));
+        const TermParams tp{0.0, beta, 1.0, 1.0, landmark_weight};
+        assemble(ctx, tp);
+        if (out_K) {
+            std::vector<double> kdev(16 * static_cast<size_t>(ctx->dp.nnzb));
+            NRR_CUDA_CHECK(cudaMemcpyAsync(kdev.data(), ctx->K.p, sizeof(double) * kdev.size(), cudaMemcpyDeviceToHost,
+                                           ctx->stream));
+            sync(ctx);
+            k_rows_to_node(ctx, kdev.data(), out_K);
+        }
+        if (out_B) {
+            launch_nodemajor_to_colmajor(ctx->B.p, ctx->xnext.p, N, ctx->stream);
+            ++ctx->launches;
+            NRR_CUDA_CHECK(cudaMemcpyAsync(out_B, ctx->xnext.p, sizeof(double) * 12 * N, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        sync(ctx);
+    });
+}
+
+int nrr_solve(nrr_ctx* ctx, const double* K, const double* B, const double* X0, double* out_X) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        require_problem(ctx);
+        const int N = ctx->N;
+        if (K) {
+            std::vector<double> krow(16 * static_cast<size_t>(ctx->dp.nnzb));
+            k_node_to_rows(ctx, K, krow.data());
+            NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->K.p, krow.data(), sizeof(double) * krow.size(), cudaMemcpyHostToDevice,
+                                           ctx->stream));
+            sync(ctx);
+        }
+        if (B) {
+            DevBuf<double> db;
+            db.upload(B, 12 * static_cast<size_t>(N), ctx->stream);
+            launch_colmajor_to_nodemajor(db.p, ctx->B.p, N, ctx->stream);
+            ++ctx->launches;
+            sync(ctx);
+        }
+        if (X0) {
+            DevBuf<double> dx;
+            dx.upload(X0, 12 * static_cast<size_t>(N), ctx->stream);
+            launch_colmajor_to_nodemajor(dx.p, ctx->x.p, N, ctx->stream);
+            ++ctx->launches;
+            sync(ctx);
+        } else {
+            NRR_CUDA_CHECK(cudaMemsetAsync(ctx->x.p, 0, sizeof(double) * 12 * N, ctx->stream));
+        }
+        solve(ctx, ctx->x.p, ctx->xmm.p);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->h_status.p, ctx->d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+        sync(ctx);
+        check_pcg(ctx, *ctx->h_status.p);
+        if (out_X) {
+            launch_nodemajor_to_colmajor(ctx->xmm.p, ctx->xnext.p, N, ctx->stream);
+            ++ctx->launches;
+            NRR_CUDA_CHECK(cudaMemcpyAsync(out_X, ctx->xnext.p, sizeof(double) * 12 * N, cudaMemcpyDeviceToHost,
+                                           ctx->stream));
+            sync(ctx);
+        }
+    });
+}
+
 int nrr_anderson_combine(nrr_ctx* ctx, const double* G, const double* F, int32_t h, int32_t dim, int32_t m,
                          double* out, int32_t* out_rank) {
     return guarded([&] {
@@ -1233,7 +1353,7 @@ int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* 
     if (ctx->prof.n && std::getenv("NRR_PROF")) {
         long long h[10];
         cudaMemcpy(h, ctx->prof.p, sizeof(h), cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "pcg phase cycles: halo %lld spmvA %lld slotsA %lld totA %lld updB %lld slotsB %lld totB %lld - %lld exsync %lld misc %lld\n",
+        std::fprintf(stderr, "pcg phase cycles: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
                      h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
     }
     if (launches) *launches = ctx->launches;

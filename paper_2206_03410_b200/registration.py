@@ -332,6 +332,27 @@ class Context:
                                 d(Xmm) if Xmm is not None else None))
         return {"index": idx, "sqdist": sq, "energy": e4, "K": K, "B": B, "Xmm": Xmm}
 
+    def assemble(self, corr_points, w_align, w_reg, rotations, beta, landmark_weight=0.0, cfg=None, nnzb=None):
+        """SystemAssembler::fill (energy.hpp:182-228) from caller correspondences,
+        weights and rotations (N x 3 x 3); returns (K in pattern order, B 4N x 3
+        column-major flat). The system stays resident for solve()."""
+        N = self.N
+        q, wa = f64(np.asarray(corr_points).reshape(-1, 3)), f64(w_align)
+        wr = f64(w_reg) if len(w_reg) else np.zeros(1)
+        R = f64(np.asarray(rotations).reshape(N, 9))
+        K = np.zeros(16 * nnzb) if nnzb else None
+        B = np.zeros(12 * N)
+        check(self.lib.nrr_assemble(self.h, d(q), d(wa), d(wr), d(R), beta, landmark_weight,
+                                    C.byref(cfg) if cfg else None, d(K) if K is not None else None, d(B)))
+        return K, B
+
+    def solve(self, K=None, B=None, X0=None):
+        """SystemAssembler::solve (energy.hpp:233-254) on the device PCG."""
+        out = np.zeros(12 * self.N)
+        check(self.lib.nrr_solve(self.h, d(f64(K)) if K is not None else None, d(f64(B)) if B is not None else None,
+                                 d(f64(X0)) if X0 is not None else None, d(out)))
+        return out
+
     def anderson_combine(self, G, F, m):
         G, F = f64(G), f64(F)
         h, dim = G.shape
