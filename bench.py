@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=5)
+    ap.add_argument("--pcg-rtol", type=float, default=None, help="override the library default (1e-13)")
     return ap.parse_args()
 
 
@@ -227,7 +228,7 @@ def run_b200(args, dist):
     p = problem_for(args.config, dist.rank)
     g = p.graph
     n, m, N, P, sumk = p.n, len(p.target), g.node_count, g.pair_count, len(g.infl_nodes)
-    ctx = R.Context(device=dist.local)
+    ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
     ctx.set_problem(p)
     prm = ctx.init_parameters()
     cfg_kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300)
@@ -273,7 +274,7 @@ def run_b200(args, dist):
 
     # end-to-end through the C ABI with host buffers (uploads, index build,
     # init_parameters, K iterations, downloads), wall clock around the call
-    e2e_ctx = R.Context(device=dist.local)
+    e2e_ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
     cfg_e2e = R.solver_config(i_max=K, **cfg_kw)
     t0 = time.perf_counter()
     e2e_ctx.register(cfg_e2e, one_shot_problem=p)

@@ -99,7 +99,7 @@ typedef struct nrr_report_summary {
  * solves directly). The PCG stops when max|r| <= pcg_rtol*(1+max|B|) and the
  * true residual meets the reference bar 1e-8*(1+max|B|) (energy.hpp:245). */
 typedef struct nrr_solve_options {
-    double pcg_rtol;      /* default 1e-12 (AA trajectories need it) */
+    double pcg_rtol;      /* default 1e-13: AA trajectories then track the reference as long as the reference tracks itself under a change of direct-solver ordering */
     int32_t pcg_max_iter; /* default 20000 */
     int32_t record_passes;/* keep per-pass records (and NN indices if nonzero==2) */
 } nrr_solve_options;

@@ -243,9 +243,11 @@ def init_parameters(problem, cfg=None):
             "alpha_forced_zero": bool(out[5])}
 
 
-def register(problem, cfg=None, pass_cap=0, with_nn=False):
-    """register_surfaces on the oracle; returns (X, deformed, report dict)."""
+def register(problem, cfg=None, pass_cap=0, with_nn=False, ordering=0):
+    """register_surfaces on the oracle; returns (X, deformed, report dict).
+    ordering: node order of the direct solve, 0 = RCM, 1 = natural."""
     lib = load()
+    lib.oracle_set_ldlt_ordering(int(ordering))
     cfg = cfg or config()
     v = view(problem)
     n, N = len(problem.source), problem.graph.node_count

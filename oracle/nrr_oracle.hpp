@@ -661,11 +661,26 @@ struct LinearSystem {  // energy.hpp:118-121
 /// Cuthill-McKee node ordering. Stands in for Eigen::SimplicialLDLT
 /// (energy.hpp:234-238, 394): the factorization fails exactly when a pivot
 /// D_ii is exactly zero, as SimplicialLDLT's numeric factorization does.
+/// Node ordering of the direct solve: 0 = reverse Cuthill-McKee (default),
+/// 1 = natural order. The reference's Eigen SimplicialLDLT uses yet another
+/// (AMD) order; the parity tests use the spread between two valid orders as
+/// the reference's own rounding-level reproducibility.
+inline int& ldlt_ordering() {
+    static int mode = 0;
+    return mode;
+}
+
 class EnvelopeLDLT {
 public:
     void analyze(const BlockSparse& k) {
         n_nodes_ = k.nodes;
         const int N = k.nodes;
+        if (ldlt_ordering() == 1) {
+            perm_.resize(N);
+            std::iota(perm_.begin(), perm_.end(), 0);
+            finish_analysis(k);
+            return;
+        }
         // RCM over the node graph, component by component, min-degree start
         perm_.clear();
         std::vector<char> seen(N, 0);
@@ -692,6 +707,11 @@ public:
             }
         }
         std::reverse(perm_.begin(), perm_.end());
+        finish_analysis(k);
+    }
+
+    void finish_analysis(const BlockSparse& k) {
+        const int N = k.nodes;
         inv_.assign(N, 0);
         for (int i = 0; i < N; ++i) inv_[perm_[i]] = i;
         // first column (in permuted scalar order) of each permuted scalar row

@@ -313,6 +313,8 @@ struct Recorder : PassObserver {
 };
 }  // namespace
 
+void oracle_set_ldlt_ordering(int mode) { oracle::ldlt_ordering() = mode; }
+
 int oracle_register(const oracle_problem_view* p, const oracle_solver_config* c, double* out_X,
                     double* out_deformed, oracle_iteration_record* iters, int32_t iter_cap,
                     oracle_stage_record* stages, int32_t stage_cap, oracle_pass_record* passes,

@@ -98,6 +98,8 @@ int oracle_step(const oracle_problem_view* p, const double* X, const double* prm
 int oracle_anderson_combine(const double* G, const double* F, int32_t h, int32_t dim, int32_t m,
                             double* out, int32_t* out_rank);
 
+/* 0 = RCM (default), 1 = natural node order for the direct solve */
+void oracle_set_ldlt_ordering(int mode);
 int oracle_register(const oracle_problem_view* p, const oracle_solver_config* cfg, double* out_X,
                     double* out_deformed, oracle_iteration_record* iters, int32_t iter_cap,
                     oracle_stage_record* stages, int32_t stage_cap, oracle_pass_record* passes,

@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             tol = a.rtol * (1.0 + bmax);
             bar = 1e-8 * (1.0 + bmax);
             if (restarts > 0) {
-                if (rmax0 <= bar && (rmax0 <= 100.0 * tol || restarts >= 3)) {
+                if (rmax0 <= bar && (rmax0 <= a.true_factor * tol || restarts >= 3)) {
                     status_code = 1;
                     break;
                 }

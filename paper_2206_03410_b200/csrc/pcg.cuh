@@ -43,6 +43,7 @@ struct PcgArgs {
     double* part_b;       // grid*16
     PcgStatus* status;
     double rtol;
+    double true_factor;  // accept the true residual at true_factor * rtol (1+|B|max)
     int max_iter;
     int max_rows, max_kb, k_in_smem, max_ext;
     int agg_ctas, n_agg, use_coarse;

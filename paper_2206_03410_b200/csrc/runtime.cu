@@ -115,7 +115,7 @@ struct nrr_ctx {
     cudaStream_t stream = nullptr;
     int num_sms = 0;
     size_t smem_optin = 0;
-    nrr_solve_options opt{1e-12, 20000, 0};
+    nrr_solve_options opt{1e-13, 20000, 0};
     int64_t launches = 0;
     bool timing = false;
 
@@ -133,6 +133,7 @@ struct nrr_ctx {
     std::vector<int> h_row_ptr, h_col;
     std::vector<double> h_src;
     DevBuf<double> d_src, d_infl_w, d_anchor, d_node_pos, d_pair_c;
+    std::vector<double> h_anchor;  // sum_a w_a p_a per vertex (energy.hpp:150-161)
     DevBuf<double4> d_infl_f;
     DevBuf<int> d_infl_off, d_infl_node, d_pairs, d_pair_rev, d_node_pair_off, d_row_ptr, d_col, d_ub_cptr, d_cv,
         d_cea, d_ceb, d_ub_kpos, d_ub_kpos_t, d_edges, d_edge_pab, d_edge_pba, d_lm_vertex;
@@ -398,6 +399,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->d_infl_w.upload(p->infl_weights, sumk, s);
     c->d_infl_f.upload(f.data(), sumk, s);
     c->d_anchor.upload(anchor.data(), anchor.size(), s);
+    c->h_anchor = anchor;
     c->d_node_pos.upload(p->node_positions, 3 * static_cast<size_t>(N), s);
     c->d_pairs.upload(p->reg_pairs, 2 * static_cast<size_t>(P), s);
     c->d_pair_c.upload(p->reg_weights, P, s);
@@ -666,6 +668,10 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     a.part_b = c->pcg_b.p;
     a.status = c->d_status.p;
     a.rtol = c->opt.pcg_rtol;
+    {
+        const char* tf = std::getenv("NRR_PCG_TRUE_FACTOR");
+        a.true_factor = tf ? std::atof(tf) : 100.0;
+    }
     a.max_iter = c->opt.pcg_max_iter;
     a.agg_ctas = c->plan.agg_ctas;
     a.n_agg = c->plan.n_agg;
@@ -1204,7 +1210,10 @@ int nrr_assemble(nrr_ctx* ctx, const double* corr_points, const double* w_align,
             throw ConfigError("assemble: null input array");
         if (cfg_for_landmarks) upload_landmarks(ctx, *cfg_for_landmarks);
         else ctx->dp.landmarks = 0;
-        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->q.p, corr_points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+        // the assembly consumes q = u - anchor, as the NN pass writes it
+        std::vector<double> q(3 * static_cast<size_t>(n));
+        for (size_t k = 0; k < q.size(); ++k) q[k] = corr_points[k] - ctx->h_anchor[k];
+        NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->q.p, q.data(), sizeof(double) * q.size(), cudaMemcpyHostToDevice, ctx->stream));
         NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->wa.p, w_align, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
         if (P > 0)
             NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->wr.p, w_reg, sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));

@@ -221,7 +221,7 @@ class Context:
         self.n = 0
         self.N = 0
         if pcg_rtol is not None or pcg_max_iter is not None or record_passes:
-            self.set_options(pcg_rtol or 1e-12, pcg_max_iter or 20000, record_passes)
+            self.set_options(pcg_rtol or 1e-13, pcg_max_iter or 20000, record_passes)
 
     def close(self):
         if self.h:
@@ -234,7 +234,7 @@ class Context:
         except Exception:
             pass
 
-    def set_options(self, pcg_rtol=1e-12, pcg_max_iter=20000, record_passes=0):
+    def set_options(self, pcg_rtol=1e-13, pcg_max_iter=20000, record_passes=0):
         o = capi.SolveOptions(pcg_rtol, pcg_max_iter, record_passes)
         check(self.lib.nrr_ctx_set_options(self.h, C.byref(o)))
 

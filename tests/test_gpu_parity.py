@@ -247,17 +247,17 @@ def _perturbed(p, rel):
 
 
 def _aa_parity(ctx, p, kw):
-    """Anderson-accelerated runs are chaotic in floating point (SURVEY.md
-    7(iv)): a relative perturbation of 1e-12 of
-    the target (the size of the PCG-vs-LDLT solution difference) moves the
-    *reference's own* trajectory past the 1e-6 energy tolerance after some
-    iterations. The GPU must agree with the reference for at least half of that
-    reproducibility horizon (and >= 10 iterations), and the final vertices must
-    be within 1e-5 of the bbox diagonal whenever the reference is itself
-    reproducible over the whole run."""
+    """Anderson-accelerated runs are chaotic in floating point (DESIGN.md
+    'Trajectory chaos'): the *reference algorithm itself*, solved with a
+    different but equally valid direct-solver node ordering (natural instead of
+    RCM; Eigen's SimplicialLDLT uses a third one, AMD), leaves the 1e-6 energy
+    band after some number of iterations h_ref. The GPU must agree with the
+    reference for at least half of that reproducibility horizon (and >= 10
+    iterations), and the final vertices must be within 1e-5 of the bbox
+    diagonal whenever the reference is itself reproducible over the whole run."""
     Xg, vg, rg = ctx.register(R.solver_config(**kw), one_shot_problem=p)
     Xo, vo, ro = O.register(p, O.config(**kw))
-    Xs, vs, rs = O.register(_perturbed(p, 1e-12), O.config(**kw))
+    Xs, vs, rs = O.register(p, O.config(**kw), ordering=1)
     eg, eo, es = _trace(rg), _trace(ro), _trace(rs)
     h_ref = _horizon(es, eo)
     h_gpu = _horizon(eg, eo)
