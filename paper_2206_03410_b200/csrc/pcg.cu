@@ -55,6 +55,112 @@ __device__ __forceinline__ void node_offset(const PcgArgs& a, int node, double d
     for (int k = 0; k < 3; ++k) d[k] = a.node_pos[3 * node + k] - a.agg_center[3 * g + k];
 }
 
+// ---------------------------------------------------------------- blocked Gauss-Jordan
+// In-place inverse of nm SPD matrices held in shared memory (matrix k: n_k x
+// n_k with n_k = 4 * blocks_k, leading dimension ld, base A + k * msz), all
+// processed together by the whole CTA, 4 pivots (one node block) at a time:
+//   P = A_TT^{-1} (4x4, one thread per matrix; a pivot <= drop * dmax_k drops
+//       that mode: zero row and column),
+//   R = P A_T:,  C = A_:T,
+//   A_ij -= C_i R_j,  A_iT = -C_i P,  A_Tj = R_j,  A_TT = P.
+// Three barriers per block step; every element update is a rank-4 FMA chain.
+// Fixed operation order: deterministic. Scratch: pb[nm*16], cb[nm*4*ld] (C
+// rows), rb[nm*4*ld] (R), blocks[nm] (4x4 blocks per matrix), dmax[nm].
+__device__ void block_gj_inverse(double* A, int nm, const int* blocks, int ld, size_t msz, double* pb, double* cb,
+                                 double* rb, const double* dmax, double drop) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    int nb_max = 0, rows_total = 0;
+    for (int k = 0; k < nm; ++k) {
+        nb_max = max(nb_max, blocks[k]);
+        rows_total += 4 * blocks[k];
+    }
+    for (int T = 0; T < nb_max; ++T) {
+        const int t0 = 4 * T;
+        // phase 1: P per matrix (thread k), raw C and row block T into cb / rb
+        if (threadIdx.x < nm && T < blocks[threadIdx.x]) {
+            const int k = threadIdx.x;
+            const double* Ak = A + k * msz;
+            double m[4][4], inv[4][4];
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) {
+                    m[r][c] = Ak[(t0 + r) * ld + t0 + c];
+                    inv[r][c] = r == c ? 1.0 : 0.0;
+                }
+            bool live[4];
+            for (int q = 0; q < 4; ++q) {
+                const double piv = m[q][q];
+                live[q] = piv > drop * dmax[k];
+                const double d = live[q] ? 1.0 / piv : 0.0;
+                for (int c = 0; c < 4; ++c) {
+                    m[q][c] *= d;
+                    inv[q][c] *= d;
+                }
+                for (int r = 0; r < 4; ++r) {
+                    if (r == q) continue;
+                    const double f = m[r][q];
+                    for (int c = 0; c < 4; ++c) {
+                        m[r][c] -= f * m[q][c];
+                        inv[r][c] -= f * inv[q][c];
+                    }
+                }
+            }
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) pb[k * 16 + r * 4 + c] = (live[r] && live[c]) ? inv[r][c] : 0.0;
+        }
+        for (int gi = threadIdx.x; gi < rows_total; gi += blockDim.x) {
+            int k = 0, base = 0;
+            while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
+            if (T >= blocks[k]) continue;
+            const int i = gi - base;
+            const double* Ai = A + k * msz + static_cast<size_t>(i) * ld;
+            for (int s = 0; s < 4; ++s) {
+                cb[k * 4 * ld + s * ld + i] = Ai[t0 + s];                           // C[i][s], stored s-major
+                rb[k * 4 * ld + s * ld + i] = A[k * msz + static_cast<size_t>(t0 + s) * ld + i];  // row T+s, column i
+            }
+        }
+        __syncthreads();
+        // phase 2: R = P * (row block), in place in rb
+        for (int gi = threadIdx.x; gi < rows_total; gi += blockDim.x) {
+            int k = 0, base = 0;
+            while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
+            if (T >= blocks[k]) continue;
+            const int j = gi - base;
+            double* rk = rb + k * 4 * ld;
+            const double* P = pb + k * 16;
+            const double x0 = rk[j], x1 = rk[ld + j], x2 = rk[2 * ld + j], x3 = rk[3 * ld + j];
+            for (int r = 0; r < 4; ++r) rk[r * ld + j] = P[r * 4] * x0 + P[r * 4 + 1] * x1 + P[r * 4 + 2] * x2 + P[r * 4 + 3] * x3;
+        }
+        __syncthreads();
+        // phase 3: rank-4 update, one warp per row, lanes over columns
+        for (int gi = w; gi < rows_total; gi += nw) {
+            int k = 0, base = 0;
+            while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
+            if (T >= blocks[k]) continue;
+            const int i = gi - base, nk = 4 * blocks[k];
+            double* Ai = A + k * msz + static_cast<size_t>(i) * ld;
+            const double* ck = cb + k * 4 * ld;
+            const double* rk = rb + k * 4 * ld;
+            const double* P = pb + k * 16;
+            const bool in_t = i >= t0 && i < t0 + 4;
+            const double c0 = ck[i], c1 = ck[ld + i], c2 = ck[2 * ld + i], c3 = ck[3 * ld + i];
+            for (int j = lane; j < nk; j += 32) {
+                const bool jt = j >= t0 && j < t0 + 4;
+                double v;
+                if (in_t && jt) v = P[(i - t0) * 4 + (j - t0)];
+                else if (in_t) v = rk[(i - t0) * ld + j];
+                else if (jt) {
+                    const int q = j - t0;
+                    v = -(c0 * P[q] + c1 * P[4 + q] + c2 * P[8 + q] + c3 * P[12 + q]);
+                } else {
+                    v = Ai[j] - (c0 * rk[j] + c1 * rk[ld + j] + c2 * rk[2 * ld + j] + c3 * rk[3 * ld + j]);
+                }
+                Ai[j] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- coarse setup
 // CTA c: partial[c][k][h*4+l] = sum over its rows a and blocks (a,b) with b in
 // aggregate h of psi_k(a)^T K_ab psi_l(b). The CTA's blocks are first staged
@@ -112,16 +218,24 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_invert_kernel(PcgArgs a
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nc = 4 * a.n_agg;
     double* A = reinterpret_cast<double*>(smem_raw);  // nc*nc
-    double* colk = A + nc * nc;                       // nc
-    double* rowk = colk + nc;                         // nc
-    __shared__ double s_dmax;
+    double* colk = A + nc * nc;                       // 4 * nc
+    double* rowk = colk + 4 * nc;                     // 4 * nc
+    __shared__ double s_dmax, s_pb[16];
+    __shared__ int s_blocks;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int i = w; i < nc; i += nw) {
         const int g = i >> 2, k = i & 3;
         for (int j = lane; j < nc; j += 32) {
             double sum = 0.0;
-            for (int cc = g * a.agg_ctas; cc < min((g + 1) * a.agg_ctas, grid); ++cc)
-                sum += partial[(static_cast<size_t>(cc) * 4 + k) * nc + j];
+            const int c0 = g * a.agg_ctas, c1 = min((g + 1) * a.agg_ctas, grid);
+            for (int cb = c0; cb < c1; cb += 8) {  // 8 loads in flight, summed in CTA order
+                double x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    x[u] = cb + u < c1 ? __ldcg(partial + (static_cast<size_t>(cb + u) * 4 + k) * nc + j) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) sum += x[u];
+            }
             A[i * nc + j] = sum;
         }
     }
@@ -137,40 +251,75 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_invert_kernel(PcgArgs a
         double m = 0.0;
         for (int i = 0; i < nc; ++i) m = fmax(m, fabs(A[i * nc + i]));
         s_dmax = m;
+        s_blocks = nc / 4;
     }
     __syncthreads();
-    const double drop = 1e-12 * s_dmax;
-    for (int k = 0; k < nc; ++k) {
-        const double piv = A[k * nc + k];
-        const bool ok = piv > drop;
-        const double d = ok ? 1.0 / piv : 0.0;
-        for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-            colk[i] = A[i * nc + k];
-            rowk[i] = A[k * nc + i];
-        }
-        __syncthreads();
-        for (int i = w; i < nc; i += nw) {
-            const double ci = colk[i];
-            double* Ai = A + i * nc;
-            for (int j = lane; j < nc; j += 32) {
-                double v;
-                if (!ok) v = (i == k || j == k) ? 0.0 : Ai[j];
-                else if (i == k) v = j == k ? d : rowk[j] * d;
-                else if (j == k) v = -ci * d;
-                else v = Ai[j] - ci * rowk[j] * d;
-                Ai[j] = v;
-            }
-        }
-        __syncthreads();
-    }
+    block_gj_inverse(A, 1, &s_blocks, nc, 0, s_pb, colk, rowk, &s_dmax, 1e-12);
     for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) inv[o] = A[o];
+}
+
+// ---------------------------------------------------------------- subdomain inverses
+// CTA c (same row partition as the PCG grid): the CTA's rows are split into
+// chunks of at most sub_rows consecutive (RCB-local) nodes; M_k = exact
+// inverse of each chunk's 4s x 4s diagonal block of K (blocked Gauss-Jordan,
+// block_gj_inverse), written to out[c][k][4s x sub_ld].
+constexpr int kInvThreads = 1024;
+__global__ void __launch_bounds__(kInvThreads, 1) sub_invert_kernel(PcgArgs a, double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int cta = blockIdx.x;
+    const int r0 = a.row_begin[cta], r1 = a.row_begin[cta + 1], nrows = r1 - r0;
+    const int S = a.sub_rows, ld = a.sub_ld, nch = (nrows + S - 1) / S;
+    const size_t msz = static_cast<size_t>(4) * S * ld;
+    double* A = reinterpret_cast<double*>(smem_raw);          // nch * msz
+    double* cb = A + nch * msz;                               // nch * 4 * ld
+    double* rb = cb + static_cast<size_t>(nch) * 4 * ld;       // nch * 4 * ld
+    double* pb = rb + static_cast<size_t>(nch) * 4 * ld;       // nch * 16
+    double* dmax = pb + 16 * nch;                             // nch
+    int* cstart = reinterpret_cast<int*>(dmax + nch);         // nch + 1
+    int* blocks = cstart + nch + 1;                           // nch
+    for (int k = threadIdx.x; k <= nch; k += blockDim.x) cstart[k] = (k * nrows) / nch;
+    for (size_t i = threadIdx.x; i < nch * msz; i += blockDim.x) A[i] = 0.0;
+    __syncthreads();
+    // scatter the own-row K blocks that fall inside the row's chunk
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int lr = w; lr < nrows; lr += nw) {
+        int k = 0;
+        while (cstart[k + 1] <= lr) ++k;
+        const int st = cstart[k], en = cstart[k + 1];
+        const int j = r0 + lr;
+        for (int t = a.row_ptr[j] * 16 + lane; t < a.row_ptr[j + 1] * 16; t += 32) {
+            const int b = t >> 4, e = t & 15;
+            const int cl = a.colx[b];  // own rows come first in the CTA operand order
+            if (cl >= st && cl < en) A[k * msz + ((lr - st) * 4 + (e >> 2)) * ld + (cl - st) * 4 + (e & 3)] = a.K[t];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nch) {
+        const int k = threadIdx.x;
+        blocks[k] = cstart[k + 1] - cstart[k];
+        double m = 0.0;
+        for (int q = 0; q < 4 * blocks[k]; ++q) m = fmax(m, fabs(A[k * msz + static_cast<size_t>(q) * ld + q]));
+        dmax[k] = m;
+    }
+    __syncthreads();
+    block_gj_inverse(A, nch, blocks, ld, msz, pb, cb, rb, dmax, 1e-13);
+    double* o = out + static_cast<size_t>(cta) * a.sub_chunks * msz;
+    for (int gi = w; gi < 4 * nrows; gi += nw) {
+        int k = 0, base = 0;
+        while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
+        const int i = gi - base, nk = 4 * blocks[k];
+        for (int jj = lane; jj < nk; jj += 32) o[k * msz + static_cast<size_t>(i) * ld + jj] = A[k * msz + static_cast<size_t>(i) * ld + jj];
+    }
 }
 
 // ---------------------------------------------------------------- PCG
 struct Shared {
     double* K;       // nkb*16
     int* col;        // nkb
-    double* M;       // nrows*16 block-Jacobi inverses
+    double* Minv;    // per subdomain chunk: dense inverse of its 4s x 4s diagonal block (leading dim sub_ld)
+    double* zz;      // nrows*12: M_sub r
+    int* cstart;     // chunk row ranges [cstart[k], cstart[k+1])
+    int* rchunk;     // own row -> chunk
     double* rex;     // nrows*12 exchange of r
     double* off;     // nrows*3 node offsets to the aggregate centre
     double* cinv;    // 4 x nc rows of K0^-1 for the own aggregate
@@ -243,17 +392,24 @@ __device__ __forceinline__ void block_partials(const double* vals, int nq, doubl
     __syncthreads();
 }
 
-// grid totals of slots [0, nq) (sum or max per mask) into bcast; one warp per slot
+// grid totals of slots [0, nq) (sum or max per mask) into bcast; one warp per
+// slot. All of a lane's partials are loaded before any is combined (the grid
+// is at most kMaxGridLoads*32 CTAs), so the reads cost one L2 round trip.
+constexpr int kMaxGridLoads = 5;  // 160 CTAs
 __device__ __forceinline__ void grid_totals(const double* __restrict__ part, int G, double* bcast, int nq,
                                             unsigned max_mask) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (w < nq) {
         const bool mx = (max_mask >> w) & 1u;
-        double v = 0.0;
-        for (int g = lane; g < G; g += 32) {
-            const double x = __ldcg(part + g * kQ + w);
-            v = mx ? fmax(v, x) : v + x;
+        double x[kMaxGridLoads];
+#pragma unroll
+        for (int i = 0; i < kMaxGridLoads; ++i) {
+            const int g = lane + 32 * i;
+            x[i] = g < G ? __ldcg(part + g * kQ + w) : 0.0;
         }
+        double v = x[0];
+#pragma unroll
+        for (int i = 1; i < kMaxGridLoads; ++i) v = mx ? fmax(v, x[i]) : v + x[i];
         v = mx ? warp_max(v) : warp_sum(v);
         if (lane == 0) bcast[w] = v;
     }
@@ -261,13 +417,24 @@ __device__ __forceinline__ void grid_totals(const double* __restrict__ part, int
 
 // per-aggregate sums of the 12 Psi^T slots [s0, s0+12) into out[nc x 3]:
 // out[(g*4+k)*3 + c] = sum over the aggregate's CTAs of part[cta][s0 + k*3 + c]
+// (fixed order). Runs on the warps after the grid_totals warps (w >= 4) so
+// both reductions overlap; loads are issued 8 at a time before combining.
 __device__ __forceinline__ void aggregate_sums(const PcgArgs& a, const double* __restrict__ part, int G, int s0,
                                                double* out) {
     const int nc = 4 * a.n_agg;
-    for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) {
+    const int first = 4 * 32;
+    if (static_cast<int>(threadIdx.x) < first) return;
+    for (int o = threadIdx.x - first; o < nc * 3; o += blockDim.x - first) {
         const int g = o / 12, kc = o % 12;
+        const int c0 = g * a.agg_ctas, c1 = min((g + 1) * a.agg_ctas, G);
         double s = 0.0;
-        for (int c = g * a.agg_ctas; c < min((g + 1) * a.agg_ctas, G); ++c) s += __ldcg(part + c * kQ + s0 + kc);
+        for (int cb = c0; cb < c1; cb += 8) {
+            double x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = cb + i < c1 ? __ldcg(part + (cb + i) * kQ + s0 + kc) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s += x[i];
+        }
         out[o] = s;
     }
 }
@@ -275,6 +442,16 @@ __device__ __forceinline__ void aggregate_sums(const PcgArgs& a, const double* _
 template <int EPT>
 __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     cg::grid_group grid = cg::this_grid();
+    const long long t_entry = clock64();
+    long long t_probe = t_entry;
+    const bool sprof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    auto probe = [&](int slot) {
+        if (sprof) {
+            const long long t = clock64();
+            a.prof[slot] += t - t_probe;
+            t_probe = t;
+        }
+    };
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int cta = blockIdx.x, G = gridDim.x;
     const int r0 = a.row_begin[cta], r1 = a.row_begin[cta + 1];
@@ -291,8 +468,14 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         p += kQ;
         sh.y = p;
         p += 16;
-        sh.M = p;
-        p += 16 * a.max_rows;
+        sh.Minv = p;  // offset 32*kQ + kQ + 16 doubles: even -> 16-byte aligned
+        p += static_cast<size_t>(a.sub_chunks) * 4 * a.sub_rows * a.sub_ld;
+        sh.zz = p;
+        p += 12 * a.max_rows;
+        sh.cstart = reinterpret_cast<int*>(p);
+        p += (a.sub_chunks + 2) / 2;
+        sh.rchunk = reinterpret_cast<int*>(p);
+        p += (a.max_rows + 1) / 2;
         sh.rex = p;
         p += 12 * a.max_rows;
         sh.off = p;
@@ -305,6 +488,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         p += 3 * kCoarseMax;
         sh.ext = p;
         p += 12 * static_cast<size_t>(a.max_ext);
+        if ((p - reinterpret_cast<double*>(smem_raw)) & 1) ++p;  // 16-byte aligned K
         if (a.k_in_smem) {
             sh.K = p;
             p += 16 * static_cast<size_t>(a.max_kb);
@@ -320,6 +504,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         for (int i = threadIdx.x; i < nkb * 8; i += blockDim.x) dst[i] = src[i];
         for (int i = threadIdx.x; i < nkb; i += blockDim.x) sh.col[i] = a.colx[kb0 + i];
     }
+    probe(10);  // K -> smem issued
     if (a.use_coarse) {
         for (int i = threadIdx.x; i < 4 * nc; i += blockDim.x) {
             const int k = i / nc, j = i % nc;
@@ -356,25 +541,25 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                 l[r * 4 + c] = v / d;
             }
         }
-        double* M = sh.M + lr * 16;
-        if (!ok) {
-            atomicMin(&a.status->fail_node, node);
-            for (int t = 0; t < 16; ++t) M[t] = 0.0;
-            continue;
-        }
-        for (int e = 0; e < 4; ++e) {
-            double y[4];
-            for (int r = 0; r < 4; ++r) {
-                double v = (r == e) ? 1.0 : 0.0;
-                for (int t = 0; t < r; ++t) v -= l[r * 4 + t] * y[t];
-                y[r] = v / l[r * 4 + r];
-            }
-            for (int r = 3; r >= 0; --r) {
-                double v = y[r];
-                for (int t = r + 1; t < 4; ++t) v -= l[t * 4 + r] * y[t];
-                y[r] = v / l[r * 4 + r];
-            }
-            for (int r = 0; r < 4; ++r) M[r * 4 + e] = y[r];
+        if (!ok) atomicMin(&a.status->fail_node, node);
+    }
+    probe(11);  // coarse rows + 4x4 checks
+    // ---- subdomain block Jacobi: M_k (dense inverses of the CTA's chunk
+    // diagonal blocks, sub_invert_kernel) staged into shared memory
+    const int sub_ld = a.sub_ld;
+    const size_t sub_msz = static_cast<size_t>(4) * a.sub_rows * sub_ld;
+    {
+        const int S = a.sub_rows;
+        const int nch = (nrows + S - 1) / S;
+        for (int k = threadIdx.x; k <= nch; k += blockDim.x) sh.cstart[k] = (k * nrows) / nch;
+        const double2* src = reinterpret_cast<const double2*>(a.sub_inv + static_cast<size_t>(cta) * a.sub_chunks * sub_msz);
+        double2* dst = reinterpret_cast<double2*>(sh.Minv);
+        for (size_t i = threadIdx.x; i < nch * sub_msz / 2; i += blockDim.x) dst[i] = __ldcg(src + i);
+        __syncthreads();
+        for (int lr = threadIdx.x; lr < nrows; lr += blockDim.x) {
+            int k = 0;
+            while (sh.cstart[k + 1] <= lr) ++k;
+            sh.rchunk[lr] = k;
         }
     }
     __syncthreads();
@@ -414,16 +599,33 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         if (lr < 0) return 0.0;
         const int j = r0 + lr;
         const int b0 = a.row_ptr[j] - kb0, b1 = a.row_ptr[j + 1] - kb0;
-        double acc = 0.0;
-        for (int b = b0; b < b1; ++b) {
+        // two independent chains (even / odd blocks) halve the FMA latency chain
+        double acc0 = 0.0, acc1 = 0.0;
+        int b = b0;
+        for (; b + 1 < b1; b += 2) {
+            const int c0 = sh.col[b], c1 = sh.col[b + 1];
+            const double* k0 = sh.K + static_cast<size_t>(b) * 16 + my_r * 4;
+            const double* k1 = k0 + 16;
+            const double* v0 = sh.ext + c0 * 12 + my_c;
+            const double* v1 = sh.ext + c1 * 12 + my_c;
+            acc0 = fma(k0[0], v0[0], acc0);
+            acc1 = fma(k1[0], v1[0], acc1);
+            acc0 = fma(k0[1], v0[3], acc0);
+            acc1 = fma(k1[1], v1[3], acc1);
+            acc0 = fma(k0[2], v0[6], acc0);
+            acc1 = fma(k1[2], v1[6], acc1);
+            acc0 = fma(k0[3], v0[9], acc0);
+            acc1 = fma(k1[3], v1[9], acc1);
+        }
+        if (b < b1) {
             const double* kk = sh.K + static_cast<size_t>(b) * 16 + my_r * 4;
             const double* vv = sh.ext + sh.col[b] * 12 + my_c;
-            acc = fma(kk[0], vv[0], acc);
-            acc = fma(kk[1], vv[3], acc);
-            acc = fma(kk[2], vv[6], acc);
-            acc = fma(kk[3], vv[9], acc);
+            acc0 = fma(kk[0], vv[0], acc0);
+            acc0 = fma(kk[1], vv[3], acc0);
+            acc0 = fma(kk[2], vv[6], acc0);
+            acc0 = fma(kk[3], vv[9], acc0);
         }
-        return acc;
+        return acc0 + acc1;
     };
     // Psi^T contribution of the thread's elements (own column): 4 mode sums
     auto psi_acc = [&](int k, double v, double ps[4]) {
@@ -469,6 +671,48 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         for (int k = 0; k < EPT; ++k)
             if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = rr[k];
         __syncthreads();
+        // zz = M_sub r: 4 threads per scalar row i split the chunk's columns,
+        // butterfly-combined in a fixed order
+        for (int t = threadIdx.x; t < 16 * nrows; t += blockDim.x) {
+            const int i = t >> 2, q = t & 3, lr = i >> 2;
+            const int ch = sh.rchunk[lr], st = sh.cstart[ch];
+            const int nk = 4 * (sh.cstart[ch + 1] - st);
+            const double* m = sh.Minv + ch * sub_msz + static_cast<size_t>(i - 4 * st) * sub_ld;
+            const double* rv = sh.rex + 12 * st;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+            int j = q;
+            for (; j + 4 < nk; j += 8) {
+                const double mj = m[j], mk = m[j + 4];
+                a0 = fma(mj, rv[3 * j], a0);
+                b0 = fma(mk, rv[3 * j + 12], b0);
+                a1 = fma(mj, rv[3 * j + 1], a1);
+                b1 = fma(mk, rv[3 * j + 13], b1);
+                a2 = fma(mj, rv[3 * j + 2], a2);
+                b2 = fma(mk, rv[3 * j + 14], b2);
+            }
+            if (j < nk) {
+                const double mj = m[j];
+                a0 = fma(mj, rv[3 * j], a0);
+                a1 = fma(mj, rv[3 * j + 1], a1);
+                a2 = fma(mj, rv[3 * j + 2], a2);
+            }
+            a0 += b0;
+            a1 += b1;
+            a2 += b2;
+            const unsigned grp = 0xFu << (threadIdx.x & 28);
+            a0 += __shfl_xor_sync(grp, a0, 1);
+            a1 += __shfl_xor_sync(grp, a1, 1);
+            a2 += __shfl_xor_sync(grp, a2, 1);
+            a0 += __shfl_xor_sync(grp, a0, 2);
+            a1 += __shfl_xor_sync(grp, a1, 2);
+            a2 += __shfl_xor_sync(grp, a2, 2);
+            if (q == 0) {
+                sh.zz[3 * i] = a0;
+                sh.zz[3 * i + 1] = a1;
+                sh.zz[3 * i + 2] = a2;
+            }
+        }
+        __syncthreads();
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
             if (el_row[k] < 0) {
@@ -476,9 +720,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                 continue;
             }
             const int lr = el_row[k];
-            const double* M = sh.M + lr * 16 + my_r * 4;
-            const double* rv = sh.rex + lr * 12 + my_c;
-            double z = M[0] * rv[0] + M[1] * rv[3] + M[2] * rv[6] + M[3] * rv[9];
+            double z = sh.zz[lr * 12 + my_rc];
             if (a.use_coarse) {
                 if (my_r < 3) z += sh.y[my_r * 3 + my_c];
                 else
@@ -494,7 +736,9 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             if (el_row[k] >= 0) sh.ext[el_row[k] * 12 + my_rc] = zr[k];
     };
 
+    probe(13);  // Gauss-Jordan
     grid.sync();  // fail flags visible
+    probe(14);
     if (__ldcg(&a.status->fail_node) != 0x7fffffff) return;
 
     int it = 0, restarts = 0;
@@ -504,6 +748,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     int status_code = 0;  // 1 converged, 2 indefinite, 3 max iter
     const bool prof = a.prof != nullptr && cta == 0 && threadIdx.x == 0;
     long long tp = clock64(), acc_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long t_setup = tp - t_entry;
     auto mark = [&](int slot) {
         if (prof) {
             const long long t = clock64();
@@ -684,6 +929,10 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         if (el_row[k] >= 0) a.X[el_g[k]] = xr[k];
     if (prof)
         for (int k = 0; k < 8; ++k) a.prof[k] += acc_t[k];
+    if (prof) {
+        a.prof[8] += t_setup;
+        a.prof[9] += 1;
+    }
     if (cta == 0 && threadIdx.x == 0) {
         a.status->iterations = it;
         a.status->code = status_code;
@@ -737,9 +986,9 @@ void rcb(RcbCtx& ctx, int lo, int hi, int g0, int g1) {
 
 void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit) {
     nodes = N;
-    grid = std::max(1, std::min(num_sms, N));
+    grid = std::max(1, std::min({num_sms, N, 32 * kMaxGridLoads}));
     const int cap_rows = (kPcgThreads * 4) / 12;
-    while ((N + grid - 1) / grid > cap_rows * 7 / 8 && grid < num_sms) ++grid;
+    while ((N + grid - 1) / grid > cap_rows * 7 / 8 && grid < std::min(num_sms, 32 * kMaxGridLoads)) ++grid;
     if ((N + grid - 1) / grid > cap_rows)
         throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 170)");
     std::vector<int> ids(N), w(N);
@@ -808,11 +1057,29 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
         ext_off[g + 1] = static_cast<int>(ext_node.size());
         max_ext = std::max(max_ext, static_cast<int>(nodes_g.size()));
     }
-    const size_t base = sizeof(double) * (32 * kQ + kQ + 16 + 32 * static_cast<size_t>(max_rows) + 10 * kCoarseMax +
-                                          12 * static_cast<size_t>(max_ext));
+    const size_t fixed = 32 * kQ + kQ + 16 + 12 * static_cast<size_t>(max_rows) /* zz */ + (max_rows + 1) / 2 +
+                         12 * static_cast<size_t>(max_rows) /* rex */ + ((3 * max_rows + 1) & ~1) + 10 * kCoarseMax +
+                         12 * static_cast<size_t>(max_ext) + 2;
     const size_t kbytes = static_cast<size_t>(max_kb) * (16 * sizeof(double) + sizeof(int));
-    k_in_smem = base + kbytes + 64 <= smem_limit;
-    smem_bytes = base + (k_in_smem ? kbytes : 0) + 64;
+    k_in_smem = sizeof(double) * fixed + kbytes + 64 <= smem_limit;
+    // largest subdomain chunk (rows per dense block-Jacobi inverse) that fits
+    auto sub_doubles = [&](int S) {
+        const int ld = sub_leading_dim(S);
+        const size_t ch = (max_rows + S - 1) / S;
+        return ch * 4 * static_cast<size_t>(S) * ld + (ch + 2) / 2;
+    };
+    int S = std::max(1, std::min(max_rows, kSubRowsMax));  // largest chunk that fits; NRR_SUB_ROWS overrides
+    if (const char* e = std::getenv("NRR_SUB_ROWS")) S = std::max(1, std::min(max_rows, std::atoi(e)));
+    const size_t kpart = k_in_smem ? kbytes : 0;
+    while (S > 1 && (sizeof(double) * (fixed + sub_doubles(S)) + kpart + 64 > smem_limit ||
+                     sizeof(double) * ((max_rows + S - 1) / S) * (4 * static_cast<size_t>(S) + 8) * sub_leading_dim(S) +
+                             1024 > smem_limit))
+        --S;
+    sub_rows = S;
+    sub_ld = sub_leading_dim(S);
+    sub_chunks = (max_rows + S - 1) / S;
+    smem_bytes = sizeof(double) * (fixed + sub_doubles(S)) + kpart + 64;
+    if (smem_bytes > smem_limit) throw ConfigError("PCG: shared-memory plan does not fit");
 }
 
 void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s) {
@@ -822,15 +1089,32 @@ void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork
     coarse_partial_kernel<<<plan.grid, kCoarseThreads, psmem, s>>>(a, w.partial);
     NRR_CUDA_CHECK(cudaGetLastError());
     const int nc = 4 * plan.n_agg;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(nc) * nc + 2 * nc);
+    const size_t smem = sizeof(double) * (static_cast<size_t>(nc) * nc + 8 * nc);
     NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     coarse_invert_kernel<<<1, kCoarseThreads, smem, s>>>(a, w.partial, w.inv, plan.grid);
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 
+void launch_sub_invert(const PcgPlan& plan, const PcgArgs& a, double* out, cudaStream_t s) {
+    const size_t ch = plan.sub_chunks;
+    const size_t smem = sizeof(double) * (ch * 4 * plan.sub_rows * plan.sub_ld + ch * 8 * plan.sub_ld + 17 * ch) +
+                        sizeof(int) * (2 * ch + 2) + 16;
+    NRR_CUDA_CHECK(cudaFuncSetAttribute(sub_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    PcgArgs b = a;
+    b.sub_rows = plan.sub_rows;
+    b.sub_ld = plan.sub_ld;
+    b.sub_chunks = plan.sub_chunks;
+    sub_invert_kernel<<<plan.grid, kInvThreads, smem, s>>>(b, out);
+    NRR_CUDA_CHECK(cudaGetLastError());
+}
+
 void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
     args.max_rows = plan.max_rows;
+    args.sub_rows = plan.sub_rows;
+    args.sub_ld = plan.sub_ld;
+    args.sub_chunks = plan.sub_chunks;
     args.max_kb = plan.max_kb;
     args.max_ext = plan.max_ext;
     args.k_in_smem = plan.k_in_smem ? 1 : 0;

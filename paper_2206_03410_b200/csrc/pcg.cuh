@@ -9,7 +9,15 @@
 namespace nrr_b200 {
 
 constexpr int kPcgThreads = 576;  // multiple of 12: (row r, column c) fixed per thread
-constexpr int kCoarseMax = 256;  // coarse dimension limit (4 modes per aggregate)
+constexpr int kCoarseMax = 256;
+constexpr int kSubRowsMax = 16;  // nodes per dense subdomain block (64 scalar rows; measured best on cfg2)
+// leading dimension of a 4s x 4s subdomain inverse: >= 4s and = 4 (mod 16), so
+// the 4 threads x 4 rows of a half-warp hit 16 distinct bank pairs
+inline int sub_leading_dim(int s) {
+    int ld = 4 * s;
+    while (ld % 16 != 4) ++ld;
+    return ld;
+}  // coarse dimension limit (4 modes per aggregate)
 
 struct PcgStatus {
     int fail_node;   // first node whose 4x4 diagonal block is not PD (INT_MAX = none)
@@ -39,6 +47,7 @@ struct PcgArgs {
     const double* agg_center;  // n_agg*3
     const int* node_agg;  // N: aggregate of node
     const double* coarse_inv;  // n_c x n_c
+    const double* sub_inv;     // grid x sub_chunks x (4 sub_rows x sub_ld): subdomain inverses
     double* part_a;       // grid*16
     double* part_b;       // grid*16
     PcgStatus* status;
@@ -46,6 +55,7 @@ struct PcgArgs {
     double true_factor;  // accept the true residual at true_factor * rtol (1+|B|max)
     int max_iter;
     int max_rows, max_kb, k_in_smem, max_ext;
+    int sub_rows, sub_ld, sub_chunks;  // subdomain block-Jacobi plan
     int agg_ctas, n_agg, use_coarse;
     long long* prof;  // optional clock64 per phase (CTA 0), accumulated
 };
@@ -53,6 +63,7 @@ struct PcgArgs {
 struct PcgPlan {
     int nodes = 0, grid = 0, ept = 1, max_rows = 0, max_kb = 0, max_ext = 0;
     int agg_ctas = 1, n_agg = 1;
+    int sub_rows = 1, sub_ld = 4, sub_chunks = 1;
     bool k_in_smem = false, use_coarse = true;
     size_t smem_bytes = 0;
     std::vector<int> row_begin;   // grid+1
@@ -74,6 +85,8 @@ struct CoarseWork {
 
 // K_0 = Psi^T K Psi partials per CTA, then one CTA sums and inverts it.
 void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s);
+// dense inverses of the subdomain diagonal blocks (one CTA per PCG CTA)
+void launch_sub_invert(const PcgPlan& plan, const PcgArgs& a, double* out, cudaStream_t s);
 void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s);
 
 }  // namespace nrr_b200

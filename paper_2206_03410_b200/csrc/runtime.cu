@@ -113,6 +113,8 @@ using namespace nrr_b200;
 struct nrr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // subdomain inverses run beside the coarse setup
+    cudaEvent_t fork = nullptr, join = nullptr;
     int num_sms = 0;
     size_t smem_optin = 0;
     nrr_solve_options opt{1e-13, 20000, 0};
@@ -143,7 +145,7 @@ struct nrr_ctx {
     // ---- per-iteration state
     DevBuf<double> x, xmm, xnext, vhat, vhat2, d2, q, wa, wr, R, K, B, Z, term_part, pcg_a, pcg_b;
     DevBuf<int> nn_idx, deg, row_begin, d_row_node, d_node_row, d_node_agg, d_colx, d_ext_off, d_ext_node;
-    DevBuf<double> d_agg_center, coarse_part, coarse_inv;
+    DevBuf<double> d_agg_center, coarse_part, coarse_inv, sub_inv;
     PcgPlan plan;
     ClusterPlan cplan;
     bool use_cluster = false;
@@ -185,6 +187,9 @@ struct nrr_ctx {
                 if (x) cudaEventDestroy(x);
         for (auto& x : pass_ev)
             if (x) cudaEventDestroy(x);
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
+        if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -473,6 +478,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         const size_t nc = 4 * static_cast<size_t>(c->plan.n_agg);
         c->coarse_part.resize(static_cast<size_t>(c->plan.grid) * 4 * nc);
         c->coarse_inv.resize(nc * nc);
+        c->sub_inv.resize(static_cast<size_t>(c->plan.grid) * c->plan.sub_chunks * 4 * c->plan.sub_rows *
+                          c->plan.sub_ld);
         c->pcg_a.resize(16 * static_cast<size_t>(c->plan.grid));
         c->pcg_b.resize(16 * static_cast<size_t>(c->plan.grid));
         d.node_row = c->d_node_row.p;
@@ -664,6 +671,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     a.agg_center = c->d_agg_center.p;
     a.node_agg = c->d_node_agg.p;
     a.coarse_inv = c->coarse_inv.p;
+    a.sub_inv = c->sub_inv.p;
     a.part_a = c->pcg_a.p;
     a.part_b = c->pcg_b.p;
     a.status = c->d_status.p;
@@ -688,7 +696,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
         ca.max_iter = c->opt.pcg_max_iter;
         if (std::getenv("NRR_PROF")) {
             if (c->prof.n == 0) {
-                c->prof.resize(10);
+                c->prof.resize(16);
                 c->prof.zero(c->stream);
             }
             ca.prof = c->prof.p;
@@ -699,15 +707,24 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     }
     if (std::getenv("NRR_PROF")) {
         if (c->prof.n == 0) {
-            c->prof.resize(10);
+            c->prof.resize(16);
             c->prof.zero(c->stream);
         }
         a.prof = c->prof.p;
     }
+    // the subdomain inverses and the coarse operator both depend on K only:
+    // run them side by side (one CTA per SM for the former, one CTA for the
+    // latter's inversion)
+    NRR_CUDA_CHECK(cudaEventRecord(c->fork, c->stream));
+    NRR_CUDA_CHECK(cudaStreamWaitEvent(c->side, c->fork, 0));
+    launch_sub_invert(c->plan, a, c->sub_inv.p, c->side);
+    NRR_CUDA_CHECK(cudaEventRecord(c->join, c->side));
+    ++c->launches;
     if (c->plan.use_coarse) {
         launch_coarse_setup(c->plan, a, CoarseWork{c->coarse_part.p, c->coarse_inv.p}, c->stream);
         c->launches += 2;
     }
+    NRR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->join, 0));
     launch_pcg(c->plan, a, c->stream);
     ++c->launches;
 }
@@ -948,6 +965,9 @@ int nrr_ctx_create(int device, nrr_ctx** out) {
         c->num_sms = prop.multiProcessorCount;
         c->smem_optin = prop.sharedMemPerBlockOptin;
         NRR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        NRR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+        NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         c->d_rec.resize(1);
         c->d_status.resize(1);
         c->deg.resize(1);
@@ -1360,10 +1380,11 @@ int nrr_debug_solver_plan(const nrr_problem_view* p, int32_t num_sms, int64_t sm
 
 int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* pcg_iters) {
     if (ctx->prof.n && std::getenv("NRR_PROF")) {
-        long long h[10];
+        long long h[16];
         cudaMemcpy(h, ctx->prof.p, sizeof(h), cudaMemcpyDeviceToHost);
         std::fprintf(stderr, "pcg phase cycles: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
                      h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+        std::fprintf(stderr, "pcg setup cycles: %lld %lld %lld %lld %lld %lld\n", h[10], h[11], h[12], h[13], h[14], h[15]);
     }
     if (launches) *launches = ctx->launches;
     if (kernel_ms6)
