@@ -44,7 +44,7 @@ namespace nrr_b200 {
 
 namespace {
 
-constexpr int kQ = 16;  // partial slots per CTA and phase
+constexpr int kQ = kPcgSlots;  // partial slots per CTA and phase
 constexpr int kCoarseThreads = 512;
 
 // coarse mode k of node a in aggregate g: [e_k; d_k] for k < 3, e_3 for k = 3,
@@ -324,7 +324,8 @@ struct Shared {
     double* off;     // nrows*3 node offsets to the aggregate centre
     double* cinv;    // 4 x nc rows of K0^-1 for the own aggregate
     double* rho;     // nc x 3 coarse residual (replicated)
-    double* ptq;     // nc x 3 aggregate sums of Psi^T q (or Psi^T r)
+    double* ptq;     // nc x 3 aggregate sums of Psi^T w (this iteration)
+    double* sig;     // nc x 3 Psi^T s (replicated recurrence)
     double* red;     // 16 warps x kQ
     double* bcast;   // kQ
     double* y;       // 12: own aggregate coarse correction
@@ -333,61 +334,71 @@ struct Shared {
 
 __device__ __forceinline__ double op2(bool mx, double a, double b) { return mx ? fmax(a, b) : a + b; }
 
-// Block reduction of the 16 per-thread slots into part[blockIdx*kQ + k]
+// Block reduction of the 32 per-thread slots into part[blockIdx*kQ + k]
 // (sum, or max for slots in max_mask). Within a warp a transpose-reduce
-// halves the vector at every butterfly level (8+4+2+1+1 shuffles instead of
-// 16x5); then one warp per slot combines the 16 warps. Fixed order.
+// halves the vector at every butterfly level (16+8+4+2+1 shuffles instead of
+// 32x5) and leaves slot l in lane l; then warps combine the per-warp totals
+// of each slot. Fixed order.
 __device__ __forceinline__ void block_partials(const double* vals, int nq, double* red, double* part,
                                                unsigned max_mask) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    double v8[8], v4[4], v2[2], v1;
+    double v16[16], v8[8], v4[4], v2[2], v1;
     int base = 0;
     {
         const bool up = lane & 16;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const double keep = up ? vals[i + 8] : vals[i], send = up ? vals[i] : vals[i + 8];
-            const int slot = (up ? 8 : 0) + i;
-            v8[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 16));
+        for (int i = 0; i < 16; ++i) {
+            const double keep = up ? vals[i + 16] : vals[i], send = up ? vals[i] : vals[i + 16];
+            const int slot = (up ? 16 : 0) + i;
+            v16[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 16));
         }
-        base += up ? 8 : 0;
+        base += up ? 16 : 0;
     }
     {
         const bool up = lane & 8;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const double keep = up ? v8[i + 4] : v8[i], send = up ? v8[i] : v8[i + 4];
-            const int slot = base + (up ? 4 : 0) + i;
-            v4[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 8));
+        for (int i = 0; i < 8; ++i) {
+            const double keep = up ? v16[i + 8] : v16[i], send = up ? v16[i] : v16[i + 8];
+            const int slot = base + (up ? 8 : 0) + i;
+            v8[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 8));
         }
-        base += up ? 4 : 0;
+        base += up ? 8 : 0;
     }
     {
         const bool up = lane & 4;
 #pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double keep = up ? v8[i + 4] : v8[i], send = up ? v8[i] : v8[i + 4];
+            const int slot = base + (up ? 4 : 0) + i;
+            v4[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 4));
+        }
+        base += up ? 4 : 0;
+    }
+    {
+        const bool up = lane & 2;
+#pragma unroll
         for (int i = 0; i < 2; ++i) {
             const double keep = up ? v4[i + 2] : v4[i], send = up ? v4[i] : v4[i + 2];
             const int slot = base + (up ? 2 : 0) + i;
-            v2[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 4));
+            v2[i] = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 2));
         }
         base += up ? 2 : 0;
     }
     {
-        const bool up = lane & 2;
+        const bool up = lane & 1;
         const double keep = up ? v2[1] : v2[0], send = up ? v2[0] : v2[1];
         const int slot = base + (up ? 1 : 0);
-        v1 = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 2));
-        base = slot;
+        v1 = op2((max_mask >> slot) & 1u, keep, __shfl_xor_sync(0xffffffffu, send, 1));
+        base = slot;  // == lane
     }
-    v1 = op2((max_mask >> base) & 1u, v1, __shfl_xor_sync(0xffffffffu, v1, 1));
-    if ((lane & 1) == 0) red[base * 32 + w] = v1;
+    red[base * 32 + w] = v1;
     __syncthreads();
-    if (w < nq) {
-        const bool mx = (max_mask >> w) & 1u;
-        double v = lane < nw ? red[w * 32 + lane] : 0.0;
+    for (int q = w; q < nq; q += nw) {
+        const bool mx = (max_mask >> q) & 1u;
+        double v = lane < nw ? red[q * 32 + lane] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v = op2(mx, v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) part[blockIdx.x * kQ + w] = v;
+        if (lane == 0) part[blockIdx.x * kQ + q] = v;
     }
     __syncthreads();
 }
@@ -420,9 +431,9 @@ __device__ __forceinline__ void grid_totals(const double* __restrict__ part, int
 // (fixed order). Runs on the warps after the grid_totals warps (w >= 4) so
 // both reductions overlap; loads are issued 8 at a time before combining.
 __device__ __forceinline__ void aggregate_sums(const PcgArgs& a, const double* __restrict__ part, int G, int s0,
-                                               double* out) {
+                                               double* out, int first_warp) {
     const int nc = 4 * a.n_agg;
-    const int first = 4 * 32;
+    const int first = first_warp * 32;
     if (static_cast<int>(threadIdx.x) < first) return;
     for (int o = threadIdx.x - first; o < nc * 3; o += blockDim.x - first) {
         const int g = o / 12, kc = o % 12;
@@ -485,6 +496,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         sh.rho = p;
         p += 3 * kCoarseMax;
         sh.ptq = p;
+        p += 3 * kCoarseMax;
+        sh.sig = p;
         p += 3 * kCoarseMax;
         sh.ext = p;
         p += 12 * static_cast<size_t>(a.max_ext);
@@ -570,7 +583,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     // local memory).
     const int nel = nrows * 12;
     const int my_rc = threadIdx.x % 12, my_r = my_rc / 3, my_c = my_rc % 3;
-    double xr[EPT], br[EPT], rr[EPT], zr[EPT], pr[EPT], qr[EPT];
+    double xr[EPT], br[EPT], rr[EPT], zr[EPT], pr[EPT];
     int el_row[EPT];
     size_t el_g[EPT];
 #pragma unroll
@@ -582,7 +595,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + my_rc;
         xr[k] = live ? a.X[el_g[k]] : 0.0;
         br[k] = live ? a.B[el_g[k]] : 0.0;
-        pr[k] = qr[k] = zr[k] = rr[k] = 0.0;
+        pr[k] = zr[k] = rr[k] = 0.0;
     }
 
     const int e0 = a.ext_off[cta], n_ext = a.ext_off[cta + 1] - e0;
@@ -741,11 +754,23 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     probe(14);
     if (__ldcg(&a.status->fail_node) != 0x7fffffff) return;
 
+    // Chronopoulos-Gear PCG: one global reduction per iteration. With u = M r
+    // and w = K u, gamma = (r,u) and delta = (w,u) give
+    //   beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev),
+    //   p = u + beta p, s = w + beta s (= K p), x += alpha p, r -= alpha s,
+    // and the coarse residual rho = Psi^T r follows rho -= alpha sigma with
+    // sigma = Psi^T s = Psi^T w + beta sigma (Psi^T w rides on the same
+    // reduction). Per iteration: SpMV + partials, grid barrier (reduction),
+    // local updates + preconditioner, grid barrier (halo of u).
     int it = 0, restarts = 0;
     double bmax = 0.0, tol = 0.0, bar = 0.0;
-    double rz[3], beta[3] = {0, 0, 0};
+    double gam[3] = {0, 0, 0}, al_prev[3] = {1, 1, 1};
+    bool first = true;
     bool need_init = true;
     int status_code = 0;  // 1 converged, 2 indefinite, 3 max iter
+    double wr[EPT], sr[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) wr[k] = sr[k] = 0.0;
     const bool prof = a.prof != nullptr && cta == 0 && threadIdx.x == 0;
     long long tp = clock64(), acc_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long t_setup = tp - t_entry;
@@ -759,7 +784,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
 
     while (true) {
         if (need_init) {
-            // r = b - K x; coarse residual rho = Psi^T r; z = M r; (r,z)
+            // r = b - K x; rho = Psi^T r; max|r|, max|B|
 #pragma unroll
             for (int k = 0; k < EPT; ++k)
                 if (el_row[k] >= 0) {
@@ -784,7 +809,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             block_partials(vals, 14, sh.red, a.part_b, 0x3u);
             grid.sync();
             grid_totals(a.part_b, G, sh.bcast, 2, 0x3u);
-            if (a.use_coarse) aggregate_sums(a, a.part_b, G, 2, sh.rho);
+            if (a.use_coarse) aggregate_sums(a, a.part_b, G, 2, sh.rho, 4);
             __syncthreads();
             const double rmax0 = sh.bcast[0];
             bmax = sh.bcast[1];
@@ -804,117 +829,48 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                 ++restarts;
                 continue;  // verify on the true residual (need_init stays set)
             }
-            precond();
-            double rzs = 0.0;
 #pragma unroll
-            for (int k = 0; k < EPT; ++k)
-                if (el_row[k] >= 0) rzs += rr[k] * zr[k];
-            zero_vals();
-            put_col(0, rzs);
-            block_partials(vals, 3, sh.red, a.part_a, 0x0u);
-            grid.sync();
-            grid_totals(a.part_a, G, sh.bcast, 3, 0x0u);
-            __syncthreads();
-            for (int c = 0; c < 3; ++c) {
-                rz[c] = sh.bcast[c];
-                beta[c] = 0.0;
-            }
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) pr[k] = qr[k] = 0.0;
+            for (int k = 0; k < EPT; ++k) pr[k] = sr[k] = 0.0;
+            if (a.use_coarse)
+                for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) sh.sig[o] = 0.0;
+            first = true;
             need_init = false;
             __syncthreads();
+            precond();  // u = M r -> Z, own ext rows
+            grid.sync();
+            fill_halo(a.Z);
         }
-        fill_halo(a.Z);
         mark(7);
-        // ---- phase A: q = K z + beta q, p = z + beta p; (p,q), Psi^T q
+        // ---- w = K u; partials (r,u), (w,u), max|r|, Psi^T w
         {
-            const double bt = beta[my_c];
-            double pq = 0.0, ps[4] = {0, 0, 0, 0};
+            double g = 0.0, dl = 0.0, rmx = 0.0, ps[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 const double w = spmv(k);
+                wr[k] = w;
                 if (el_row[k] < 0) continue;
-                qr[k] = w + bt * qr[k];
-                pr[k] = zr[k] + bt * pr[k];
-                pq += pr[k] * qr[k];
-                psi_acc(k, qr[k], ps);
+                g += rr[k] * zr[k];
+                dl += w * zr[k];
+                rmx = fmax(rmx, fabs(rr[k]));
+                psi_acc(k, w, ps);
             }
             zero_vals();
-            put_col(0, pq);
-            if (a.use_coarse) put_psi(3, ps);
+            put_col(0, g);
+            put_col(3, dl);
+            vals[6] = rmx;
+            if (a.use_coarse) put_psi(7, ps);
         }
         mark(0);
-        block_partials(vals, a.use_coarse ? 15 : 3, sh.red, a.part_a, 0x0u);
+        block_partials(vals, a.use_coarse ? 19 : 7, sh.red, a.part_a, 1u << 6);
         mark(1);
         grid.sync();
         mark(2);
-        grid_totals(a.part_a, G, sh.bcast, 3, 0x0u);
-        if (a.use_coarse) aggregate_sums(a, a.part_a, G, 3, sh.ptq);
+        grid_totals(a.part_a, G, sh.bcast, 7, 1u << 6);
+        if (a.use_coarse) aggregate_sums(a, a.part_a, G, 7, sh.ptq, 7);
         __syncthreads();
         mark(3);
-        double alpha[3];
-        bool indefinite = false;
-        for (int c = 0; c < 3; ++c) {
-            const double pq = sh.bcast[c];
-            if (rz[c] == 0.0) {
-                alpha[c] = 0.0;
-            } else if (!(pq > 0.0)) {
-                indefinite = true;
-                alpha[c] = 0.0;
-            } else {
-                alpha[c] = rz[c] / pq;
-            }
-        }
-        if (indefinite) {
-            status_code = 2;
-            break;
-        }
-        if (a.use_coarse)
-            for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) sh.rho[o] -= alpha[o % 3] * sh.ptq[o];
-        // ---- phase B: x += alpha p, r -= alpha q, z = M r; (r,z), max|r|
-        {
-            const double al = alpha[my_c];
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
-                if (el_row[k] < 0) continue;
-                xr[k] = fma(al, pr[k], xr[k]);
-                rr[k] = fma(-al, qr[k], rr[k]);
-            }
-        }
-        __syncthreads();  // rho updated before the coarse solve
-        precond();
-        {
-            double rzs = 0.0, rmx = 0.0;
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
-                if (el_row[k] < 0) continue;
-                rzs += rr[k] * zr[k];
-                rmx = fmax(rmx, fabs(rr[k]));
-            }
-            zero_vals();
-            put_col(0, rzs);
-            vals[3] = rmx;
-        }
-        mark(4);
-        block_partials(vals, 4, sh.red, a.part_b, 0x8u);
-        mark(5);
-        grid.sync();
-        mark(6);
-        grid_totals(a.part_b, G, sh.bcast, 4, 0x8u);
-        __syncthreads();
-        double rzn[3] = {sh.bcast[0], sh.bcast[1], sh.bcast[2]};
-        const double rmax = sh.bcast[3];
-        __syncthreads();
-        ++it;
-        for (int c = 0; c < 3; ++c) {
-            beta[c] = rz[c] != 0.0 ? rzn[c] / rz[c] : 0.0;
-            rz[c] = rzn[c];
-        }
-        if (!isfinite(rz[0] + rz[1] + rz[2])) {
-            status_code = 2;
-            break;
-        }
-        if (rmax <= tol) {
+        const double rmax = sh.bcast[6];
+        if (rmax <= tol) {  // recursive residual converged: verify on the true residual
             ++restarts;
             need_init = true;
             continue;
@@ -923,6 +879,56 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             status_code = 3;
             break;
         }
+        double al[3], bt[3];
+        bool indefinite = false;
+        for (int c = 0; c < 3; ++c) {
+            const double g = sh.bcast[c], d = sh.bcast[3 + c];
+            bt[c] = (first || gam[c] == 0.0) ? 0.0 : g / gam[c];
+            const double den = bt[c] == 0.0 ? d : d - bt[c] * g / al_prev[c];
+            if (g == 0.0) {
+                al[c] = 0.0;
+            } else if (!(den > 0.0) || !isfinite(den)) {
+                indefinite = true;
+                al[c] = 0.0;
+            } else {
+                al[c] = g / den;
+            }
+            gam[c] = g;
+            if (al[c] != 0.0) al_prev[c] = al[c];
+        }
+        if (indefinite) {
+            status_code = 2;
+            break;
+        }
+        first = false;
+        if (a.use_coarse)
+            for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) {
+                const double sg = sh.ptq[o] + bt[o % 3] * sh.sig[o];
+                sh.sig[o] = sg;
+                sh.rho[o] -= al[o % 3] * sg;
+            }
+        // ---- p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = M r
+        {
+            const double a_c = al[my_c], b_c = bt[my_c];
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                if (el_row[k] < 0) continue;
+                pr[k] = fma(b_c, pr[k], zr[k]);
+                sr[k] = fma(b_c, sr[k], wr[k]);
+                xr[k] = fma(a_c, pr[k], xr[k]);
+                rr[k] = fma(-a_c, sr[k], rr[k]);
+            }
+        }
+        __syncthreads();  // rho updated before the coarse solve
+        precond();
+        mark(4);
+        ++it;
+        // u of the neighbours visible (a neighbour-only flag barrier was
+        // measured slower: the skew then piles up at the reduction barrier)
+        grid.sync();
+        mark(5);
+        fill_halo(a.Z);
+        mark(6);
     }
 #pragma unroll
     for (int k = 0; k < EPT; ++k)
@@ -1058,7 +1064,7 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
         max_ext = std::max(max_ext, static_cast<int>(nodes_g.size()));
     }
     const size_t fixed = 32 * kQ + kQ + 16 + 12 * static_cast<size_t>(max_rows) /* zz */ + (max_rows + 1) / 2 +
-                         12 * static_cast<size_t>(max_rows) /* rex */ + ((3 * max_rows + 1) & ~1) + 10 * kCoarseMax +
+                         12 * static_cast<size_t>(max_rows) /* rex */ + ((3 * max_rows + 1) & ~1) + 13 * kCoarseMax +
                          12 * static_cast<size_t>(max_ext) + 2;
     const size_t kbytes = static_cast<size_t>(max_kb) * (16 * sizeof(double) + sizeof(int));
     k_in_smem = sizeof(double) * fixed + kbytes + 64 <= smem_limit;
@@ -1126,6 +1132,21 @@ void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
                      : plan.ept == 2 ? reinterpret_cast<const void*>(pcg_kernel<2>)
                                      : reinterpret_cast<const void*>(pcg_kernel<4>);
     NRR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem_bytes)));
+    int per_sm = 0;
+    NRR_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPcgThreads, plan.smem_bytes));
+    if (per_sm < 1) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, fn);
+        int per_sm0 = 0, dev = 0, smsm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm0, fn, kPcgThreads, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        throw CudaError("PCG kernel does not fit one SM: blocks/SM without smem " + std::to_string(per_sm0) +
+                        ", smem/SM " + std::to_string(smsm) + ", maxThreads " + std::to_string(fa.maxThreadsPerBlock) +
+                        ", regs " + std::to_string(fa.numRegs) + ", static smem " +
+                        std::to_string(fa.sharedSizeBytes) + ", dynamic smem " + std::to_string(plan.smem_bytes) +
+                        ", local " + std::to_string(fa.localSizeBytes));
+    }
     NRR_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kPcgThreads), kargs, plan.smem_bytes, s));
 }
 

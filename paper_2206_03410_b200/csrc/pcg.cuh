@@ -8,8 +8,9 @@
 
 namespace nrr_b200 {
 
-constexpr int kPcgThreads = 576;  // multiple of 12: (row r, column c) fixed per thread
+constexpr int kPcgThreads = 384;  // multiple of 12: (row r, column c) fixed per thread; 12 warps leave 168 registers
 constexpr int kCoarseMax = 256;
+constexpr int kPcgSlots = 32;   // reduction slots per CTA in part_a / part_b
 constexpr int kSubRowsMax = 16;  // nodes per dense subdomain block (64 scalar rows; measured best on cfg2)
 // leading dimension of a 4s x 4s subdomain inverse: >= 4s and = 4 (mod 16), so
 // the 4 threads x 4 rows of a half-warp hit 16 distinct bank pairs
@@ -48,8 +49,8 @@ struct PcgArgs {
     const int* node_agg;  // N: aggregate of node
     const double* coarse_inv;  // n_c x n_c
     const double* sub_inv;     // grid x sub_chunks x (4 sub_rows x sub_ld): subdomain inverses
-    double* part_a;       // grid*16
-    double* part_b;       // grid*16
+    double* part_a;       // grid*kPcgSlots
+    double* part_b;       // grid*kPcgSlots
     PcgStatus* status;
     double rtol;
     double true_factor;  // accept the true residual at true_factor * rtol (1+|B|max)

@@ -480,8 +480,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->coarse_inv.resize(nc * nc);
         c->sub_inv.resize(static_cast<size_t>(c->plan.grid) * c->plan.sub_chunks * 4 * c->plan.sub_rows *
                           c->plan.sub_ld);
-        c->pcg_a.resize(16 * static_cast<size_t>(c->plan.grid));
-        c->pcg_b.resize(16 * static_cast<size_t>(c->plan.grid));
+        c->pcg_a.resize(kPcgSlots * static_cast<size_t>(c->plan.grid));
+        c->pcg_b.resize(kPcgSlots * static_cast<size_t>(c->plan.grid));
         d.node_row = c->d_node_row.p;
         // cluster-resident solver when the graph fits one cluster's shared memory
         c->cplan.build(p->node_positions, c->h_row_ptr.data(), c->h_col.data(), c->plan.node_row.data(), N,
