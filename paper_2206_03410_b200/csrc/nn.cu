@@ -185,12 +185,14 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
     }
     sp = 1;
     __syncwarp(gmask);
+    // prune radius: FP32 sqrt of the FP64 best, inflated by the rounding
+    // margin; refreshed only when the best changes
+    float thr = static_cast<float>(sqrt(best_d2)) * 1.000001f + delta;  // inf stays inf
     while (sp > 0) {
         --sp;
         const int code = sn[sp];
         const float bdist = sd[sp];
         __syncwarp(gmask);
-        const float thr = static_cast<float>(sqrt(best_d2)) * 1.000001f + delta;  // inf stays inf
         if (bdist > thr) continue;
         const int L = code >> 27, v = code & ((1 << 27) - 1);
         if (L == 0) {
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
                 }
             }
             if (my_d2 < best_d2 || (my_d2 == best_d2 && my_i < best_i)) {
+                if (my_d2 < best_d2) thr = static_cast<float>(sqrt(my_d2)) * 1.000001f + delta;
                 best_d2 = my_d2;
                 best_i = my_i;
             }
@@ -230,14 +233,10 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             const bool valid = exists && bd <= thr;
             const unsigned ball = (__ballot_sync(gmask, valid) >> gshift) & 0xFFu;
             const int cnt = __popc(ball);
-            // rank in descending distance (farthest pushed first, so the
-            // nearest child is popped next); every lane takes part
-            int rank = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float oj = __shfl_sync(gmask, bd, j, 8);
-                if (((ball >> j) & 1u) && j != lane && (oj > bd || (oj == bd && j < lane))) ++rank;
-            }
+            // children in Morton order (the warm-start bound is already tight,
+            // so nearest-first ordering buys little; exactness does not depend
+            // on the order)
+            const int rank = __popc(ball & ((1u << lane) - 1u));
             if (valid && sp + rank < kStack) {
                 sn[sp + rank] = (cl << 27) | c;
                 sd[sp + rank] = bd;
