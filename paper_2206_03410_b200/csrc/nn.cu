@@ -66,7 +66,19 @@ void BvhHost::build(const double* tgt, int m_) {
         }
         keys[i] = {code, i};
     }
-    std::sort(keys.begin(), keys.end());
+    // (code, index) order by a stable LSD radix sort on the 30-bit code (16 + 14
+    // bits); the input is already in index order, so ties keep it
+    {
+        std::vector<std::pair<uint32_t, int>> tmp(m);
+        for (int pass = 0; pass < 2; ++pass) {
+            const int shift = 16 * pass, bins = 1 << 16;
+            std::vector<int> cnt(bins + 1, 0);
+            for (int i = 0; i < m; ++i) ++cnt[((keys[i].first >> shift) & 0xFFFFu) + 1];
+            for (int b = 0; b < bins; ++b) cnt[b + 1] += cnt[b];
+            for (int i = 0; i < m; ++i) tmp[cnt[(keys[i].first >> shift) & 0xFFFFu]++] = keys[i];
+            keys.swap(tmp);
+        }
+    }
     const int mpad = (m + 7) / 8 * 8;
     pts.assign(mpad, make_float4(1e18f, 1e18f, 1e18f, 0.f));
     for (int k = 0; k < mpad; ++k) {

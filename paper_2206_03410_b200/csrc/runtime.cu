@@ -10,6 +10,7 @@
 // the solve status; all vectors stay resident in HBM.
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -36,7 +37,7 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0, cap = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -44,14 +45,17 @@ struct DevBuf {
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
-    void resize(size_t count) {
-        if (count == n && p) return;
+    void resize(size_t count) {  // grow-only: a context reused for another problem keeps its buffers
+        if (count <= cap && p) {
+            n = count;
+            return;
+        }
         release();
         if (count == 0) return;
         NRR_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
-        n = count;
+        n = cap = count;
     }
     void upload(const T* h, size_t count, cudaStream_t s) {
         resize(count);
@@ -261,7 +265,19 @@ void set_target(nrr_ctx* c, const double* tgt, int m) {
 }
 
 // SystemAssembler ctor (energy.hpp:139-176) + the B200 assembly plan
+struct SetupClock {  // NRR_PROF_SETUP=1: host setup phase timings on stderr
+    bool on = std::getenv("NRR_PROF_SETUP") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void lap(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "setup %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
+    SetupClock clk;
     const int n = p->n, N = p->node_count, E = p->edge_count, P = p->pair_count;
     if (n < 0 || N < 0 || E < 0 || P < 0) throw ConfigError("negative problem size");
     if (N == 0 && n > 0) throw ConfigError("deformation graph has no nodes");
@@ -289,6 +305,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
             for (int cc = 0; cc < 3; ++cc) anchor[3 * i + cc] += w * pa[cc];
         }
     }
+    clk.lap("influence constants");
     // BSR pattern: diagonal + both halves of each edge (energy.hpp:264-279)
     std::vector<std::vector<int>> cols(N);
     for (int j = 0; j < N; ++j) cols[j].push_back(j);
@@ -305,7 +322,9 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         deg[j] = static_cast<int>(cols[j].size());
     }
     // solver row order: RCB subdomains, one per CTA (pcg.cu)
+    clk.lap("pattern");
     if (N > 0) c->plan.build(p->node_positions, deg.data(), N, c->num_sms, c->smem_optin);
+    clk.lap("rcb plan");
     c->h_row_ptr.assign(N + 1, 0);
     c->h_col.clear();
     for (int r = 0; r < N; ++r) {
@@ -328,45 +347,82 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         const int b = std::max(p->edges[2 * e], p->edges[2 * e + 1]);
         edge_of_blk[find_blk(a, b)] = e;
     }
-    // contributor lists per upper block, in vertex order (the reference's program order)
+    clk.lap("bsr");
+    // contributor lists per upper block, in vertex order (the reference's
+    // program order). Vertex ranges are counted and filled by host threads;
+    // each upper block's list is the concatenation of the ranges in order,
+    // so the result does not depend on the thread count.
     const int U = N + E;
-    std::vector<int> cnt(U + 1, 0);
-    for (int i = 0; i < n; ++i) {
-        const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
-        for (int ka = k0; ka < k1; ++ka) {
-            ++cnt[p->infl_nodes[ka]];
-            for (int kb = k0; kb < k1; ++kb) {
-                const int a = p->infl_nodes[ka], b = p->infl_nodes[kb];
-                if (a >= b) continue;
-                const int blk = find_blk(a, b);
-                if (blk < 0) throw NumericalError("assemble: co-influencing node pair is not a graph edge");
-                ++cnt[N + edge_of_blk[blk]];
+    const int T = std::max(1, std::min<int>(8, static_cast<int>(std::thread::hardware_concurrency())));
+    std::vector<std::vector<int>> cnt_t(T, std::vector<int>(U, 0));
+    auto range = [&](int t) { return std::make_pair(static_cast<int>(static_cast<long long>(n) * t / T),
+                                                    static_cast<int>(static_cast<long long>(n) * (t + 1) / T)); };
+    std::vector<int> bad_pair(T, 0);
+    auto count_part = [&](int t) {
+        auto [i0, i1] = range(t);
+        std::vector<int>& cnt = cnt_t[t];
+        for (int i = i0; i < i1; ++i) {
+            const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
+            for (int ka = k0; ka < k1; ++ka) {
+                ++cnt[p->infl_nodes[ka]];
+                for (int kb = k0; kb < k1; ++kb) {
+                    const int a = p->infl_nodes[ka], b = p->infl_nodes[kb];
+                    if (a >= b) continue;
+                    const int blk = find_blk(a, b);
+                    if (blk < 0) {
+                        bad_pair[t] = 1;
+                        continue;
+                    }
+                    ++cnt[N + edge_of_blk[blk]];
+                }
             }
         }
-    }
+    };
+    auto run_parallel = [&](auto&& fn) {
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; ++t) th.emplace_back(fn, t);
+        fn(0);
+        for (auto& x : th) x.join();
+    };
+    run_parallel(count_part);
+    for (int t = 0; t < T; ++t)
+        if (bad_pair[t]) throw NumericalError("assemble: co-influencing node pair is not a graph edge");
     std::vector<int> cptr(U + 1, 0);
-    for (int u = 0; u < U; ++u) cptr[u + 1] = cptr[u] + cnt[u];
-    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+    std::vector<std::vector<int>> off_t(T, std::vector<int>(U, 0));
+    for (int u = 0; u < U; ++u) {
+        int base = cptr[u];
+        for (int t = 0; t < T; ++t) {
+            off_t[t][u] = base;
+            base += cnt_t[t][u];
+        }
+        cptr[u + 1] = base;
+    }
     std::vector<int> cv(cptr[U]), cea(cptr[U]), ceb(cptr[U]);
-    for (int i = 0; i < n; ++i) {
-        const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
-        for (int ka = k0; ka < k1; ++ka) {
-            const int a = p->infl_nodes[ka];
-            int t = fill[a]++;
-            cv[t] = i;
-            cea[t] = ka;
-            ceb[t] = ka;
-            for (int kb = k0; kb < k1; ++kb) {
-                const int b = p->infl_nodes[kb];
-                if (a >= b) continue;
-                const int u = N + edge_of_blk[find_blk(a, b)];
-                t = fill[u]++;
-                cv[t] = i;
-                cea[t] = ka;
-                ceb[t] = kb;
+    auto fill_part = [&](int t) {
+        auto [i0, i1] = range(t);
+        std::vector<int>& fill = off_t[t];
+        for (int i = i0; i < i1; ++i) {
+            const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
+            for (int ka = k0; ka < k1; ++ka) {
+                const int a = p->infl_nodes[ka];
+                int q = fill[a]++;
+                cv[q] = i;
+                cea[q] = ka;
+                ceb[q] = ka;
+                for (int kb = k0; kb < k1; ++kb) {
+                    const int b = p->infl_nodes[kb];
+                    if (a >= b) continue;
+                    const int u = N + edge_of_blk[find_blk(a, b)];
+                    q = fill[u]++;
+                    cv[q] = i;
+                    cea[q] = ka;
+                    ceb[q] = kb;
+                }
             }
         }
-    }
+    };
+    run_parallel(fill_part);
+    clk.lap("contributors");
     std::vector<int> kpos(U), kpos_t(U), eab(E), eba(E);
     for (int j = 0; j < N; ++j) kpos[j] = kpos_t[j] = find_blk(j, j);
     // directed pairs: i-major ranges, reverse index
@@ -397,6 +453,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         if ((eab[e] < 0 || eba[e] < 0) && P > 0) throw ConfigError("graph edge without reg pairs");
     }
     if (P == 0 && E > 0) throw ConfigError("graph edges without reg pairs");
+    clk.lap("pairs");
     // upload
     c->d_src.upload(p->source, 3 * static_cast<size_t>(n), s);
     c->d_infl_off.upload(p->infl_offsets, n + 1, s);
@@ -465,8 +522,10 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->deg.resize(1);
     c->d_rec.resize(1);
     c->d_status.resize(1);
+    clk.lap("uploads");
     if (N > 0) {
         c->plan.size_smem(c->h_row_ptr.data(), c->h_col.data(), c->smem_optin);
+        clk.lap("pcg smem plan");
         c->d_colx.upload(c->plan.colx.data(), c->plan.colx.size(), s);
         c->d_ext_off.upload(c->plan.ext_off.data(), c->plan.ext_off.size(), s);
         c->d_ext_node.upload(c->plan.ext_node.data(), c->plan.ext_node.size(), s);
@@ -483,11 +542,14 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->pcg_a.resize(kPcgSlots * static_cast<size_t>(c->plan.grid));
         c->pcg_b.resize(kPcgSlots * static_cast<size_t>(c->plan.grid));
         d.node_row = c->d_node_row.p;
-        // cluster-resident solver when the graph fits one cluster's shared memory
-        c->cplan.build(p->node_positions, c->h_row_ptr.data(), c->h_col.data(), c->plan.node_row.data(), N,
-                       c->smem_optin, 16);
+        // cluster-resident solver (opt-in) when the graph fits one cluster's shared memory
         const char* mode = std::getenv("NRR_PCG");
-        c->use_cluster = c->cplan.ok && mode && std::string(mode) == "cluster";
+        c->use_cluster = false;
+        if (mode && std::string(mode) == "cluster") {
+            c->cplan.build(p->node_positions, c->h_row_ptr.data(), c->h_col.data(), c->plan.node_row.data(), N,
+                           c->smem_optin, 16);
+            c->use_cluster = c->cplan.ok;
+        }
         if (c->use_cluster) {
             const ClusterPlan& cp = c->cplan;
             c->c_rank_rows.upload(cp.rank_rows.data(), cp.rank_rows.size(), s);
@@ -504,6 +566,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         }
     }
     NRR_CUDA_CHECK(cudaStreamSynchronize(s));
+    clk.lap("pcg uploads + sync");
     c->has_problem = true;
 }
 
@@ -590,9 +653,10 @@ Params init_parameters(nrr_ctx* c, const nrr_solver_config& cfg) {  // solver.hp
     sync(c);
     for (auto& d : dist) d = std::sqrt(d);
     double median = 0.0;
-    if (n > 0) {
-        std::sort(dist.begin(), dist.end());
-        median = n % 2 == 1 ? dist[n / 2] : 0.5 * (dist[n / 2 - 1] + dist[n / 2]);
+    if (n > 0) {  // the sorted-order median (solver.hpp:92-100) by selection
+        std::nth_element(dist.begin(), dist.begin() + n / 2, dist.end());
+        const double hi = dist[n / 2];
+        median = n % 2 == 1 ? hi : 0.5 * (*std::max_element(dist.begin(), dist.begin() + n / 2) + hi);
     }
     Params p;
     const double l_bar = c->src_avg;

@@ -21,7 +21,7 @@ NAN = float("nan")
 # Radius multipliers (R = mult * mean source edge length) tuned once so the
 # reference graph rule (deformation_graph.hpp:157-210) yields the node counts
 # BASELINE.json states for each synthetic config.
-GRAPH_MULT = {0: 5.0, 1: 3.7, 2: 5.0, 3: 3.3, 4: 7.2}
+GRAPH_MULT = {0: 5.0, 1: 5.5, 2: 5.0, 3: 5.9, 4: 7.2}
 
 
 @dataclass
