@@ -16,6 +16,13 @@ derived values, eps = 1e-300, so exactly `steps` iterations are accepted.
 N > 1 (torchrun): config 2 does not shard, so every rank runs
 an independent replica ("replicas only"); value = iterations of all ranks /
 max-over-ranks device time.
+
+Other configs:
+  --config 4   1M-vertex pair; with N > 1 the source vertices are sharded over
+               the ranks and K, B, energies are allreduced over NCCL every
+               pass ("strong": one registration, value = its iterations/s).
+  --config 3   256 independent 20K-vertex pairs, 50 iterations each, pairs
+               round-robin over the ranks, no communication.
 """
 import argparse
 import json
@@ -45,6 +52,8 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--pcg-rtol", type=float, default=None, help="override the library default (1e-13)")
+    ap.add_argument("--pairs", type=int, default=256, help="config 3: number of independent pairs")
+    ap.add_argument("--pair-iters", type=int, default=50, help="config 3: MM iterations per pair")
     return ap.parse_args()
 
 
@@ -79,6 +88,13 @@ class Dist:
         t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
         self.dist.all_reduce(t)
         return float(t.item())
+
+    def bcast_bytes(self, b):
+        if self.world == 1:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
 
     def close(self):
         if self.world > 1:
@@ -145,6 +161,8 @@ class ClockSampler:
 # ----------------------------------------------------------------- workload
 def problem_for(config, rank=0):
     from paper_2206_03410_b200 import registration as R
+    if config == 3:  # one pair of the batch (reference arm / CPU sample)
+        return R.make_problem(3, seed=4000)
     return R.make_problem(config)
 
 
@@ -206,7 +224,7 @@ def run_reference(args, dist):
     value, sec = cpu_baseline(p, kw, warm, steps)
     g = p.graph
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": 1e3 * sec / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config {args.config}: {p.n} source / {len(p.target)} target points, "
@@ -222,13 +240,37 @@ def run_reference(args, dist):
     dist.close()
 
 
+def metric_for(config):
+    if config == 2:
+        return METRIC
+    if config == 4:
+        return "MM iterations/s (1M-vertex source, config 4)"
+    if config == 3:
+        return "MM iterations/s (256 independent 20K-vertex pairs, config 3)"
+    return f"MM iterations/s (config {config})"
+
+
+def join_shard(R, ctx, dist, n_global):
+    """Vertex sharding (config 4, N > 1): one NCCL communicator per context."""
+    uid = dist.bcast_bytes(R.comm_unique_id() if dist.rank == 0 else None)
+    ctx.set_comm(uid, dist.world, dist.rank)
+    ctx.set_shard(n_global)
+
+
 def run_b200(args, dist):
     from paper_2206_03410_b200 import registration as R
 
-    p = problem_for(args.config, dist.rank)
+    p_full = problem_for(args.config, dist.rank)
+    sharded = args.config == 4 and dist.world > 1
+    if sharded:
+        p = R.shard_problem(p_full, *R.shard_bounds(p_full.n, dist.world, dist.rank))
+    else:
+        p = p_full
     g = p.graph
     n, m, N, P, sumk = p.n, len(p.target), g.node_count, g.pair_count, len(g.infl_nodes)
     ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
+    if sharded:
+        join_shard(R, ctx, dist, p_full.n)
     ctx.set_problem(p)
     prm = ctx.init_parameters()
     cfg_kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300)
@@ -247,7 +289,7 @@ def run_b200(args, dist):
     if acc != K:
         raise RuntimeError(f"only {acc} of {K} iterations accepted")
     max_ms = dist.max(dev_ms)
-    total_iters = dist.sum(float(acc))
+    total_iters = float(acc) if sharded else dist.sum(float(acc))  # sharded: one registration
     value = total_iters / (max_ms / 1e3)
     kms = {k: s1["kernel_ms"][k] - s0["kernel_ms"][k] for k in s1["kernel_ms"]}
     pcg_iters = s1["pcg_iterations"] - s0["pcg_iterations"]
@@ -275,13 +317,16 @@ def run_b200(args, dist):
     # end-to-end through the C ABI with host buffers (uploads, index build,
     # init_parameters, K iterations, downloads), wall clock around the call
     e2e_ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
+    if sharded:
+        join_shard(R, e2e_ctx, dist, p_full.n)
     cfg_e2e = R.solver_config(i_max=K, **cfg_kw)
+    dist.barrier()
     t0 = time.perf_counter()
     e2e_ctx.register(cfg_e2e, one_shot_problem=p)
     e2e_s = time.perf_counter() - t0
     e2e_iters = e2e_ctx.report()["total_iterations"]
     e2e_ctx.close()
-    e2e_value = dist.sum(float(e2e_iters)) / dist.max(e2e_s)
+    e2e_value = (float(e2e_iters) if sharded else dist.sum(float(e2e_iters))) / dist.max(e2e_s)
     h2d, d2h = h2d_d2h_bytes(p)
 
     cpu = None
@@ -293,13 +338,15 @@ def run_b200(args, dist):
     ctx.close()
     if dist.rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K, "warmup": W,
-            "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,
+            "warmup": W, "ms_per_step": max_ms / K, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config {args.config}: {n} source / {m} target points, {N} nodes, "
                                    f"{P} directed pairs, sum k {sumk}, fixed-count single stage (nu fixed, "
                                    "eps=1e-300), AA m=5",
-                       "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "1 GPU",
+                       "parallelism": (f"vertex-sharded x{dist.world} (NCCL allreduce of K, B, energies per pass)"
+                                       if sharded else f"replicas x{dist.world}" if dist.world > 1 else "1 GPU"),
                        "l2": "flushed (2x L2 write) before every timed iteration, outside the timed interval"
                        if not args.no_flush else "not flushed (working set < L2)"},
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -319,11 +366,68 @@ def run_b200(args, dist):
     dist.close()
 
 
+def run_pairs(args, dist):
+    """Config 3: independent pairs round-robin over the ranks (no
+    communication); every pair runs the fixed-count idiom for
+    --pair-iters iterations; value = all ranks' iterations / max-over-ranks
+    device time (problem generation and per-pair setup excluded; e2e includes
+    the per-pair uploads, index build and setup through the C ABI)."""
+    from paper_2206_03410_b200 import registration as R
+
+    mine = [q for q in range(args.pairs) if q % dist.world == dist.rank]
+    probs = [R.make_problem(3, seed=4000 + q) for q in mine]
+    ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
+    ctx.enable_timing(True)
+    dev_ms, iters, launches0 = 0.0, 0, ctx.stats()["launches"]
+    kms = None
+    dist.barrier()
+    t0 = time.perf_counter()
+    with ClockSampler(dist.local) as clocks:
+        for p in probs:
+            ctx.set_problem(p)
+            prm = ctx.init_parameters()
+            cfg = R.solver_config(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300,
+                                  i_max=args.pair_iters)
+            ctx.begin(cfg)
+            acc, done, ms = ctx.iterate(args.pair_iters)
+            ctx.finish()
+            dev_ms += ms
+            iters += acc
+            st = ctx.stats()["kernel_ms"]
+            kms = {k: (kms or {}).get(k, 0.0) + v for k, v in st.items()}
+    wall = time.perf_counter() - t0
+    dist.barrier()
+    launches = ctx.stats()["launches"] - launches0
+    ctx.close()
+    max_ms = dist.max(dev_ms)
+    total = dist.sum(float(iters))
+    e2e = total / dist.max(wall)
+    if dist.rank == 0:
+        g = probs[0].graph
+        line = {
+            "metric": metric_for(3), "value": total / (max_ms / 1e3), "unit": UNIT, "n_gpus": dist.world,
+            "steps": args.pair_iters, "warmup": 0, "ms_per_step": max_ms / max(1, iters),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config 3: {args.pairs} pairs x {probs[0].n} source points (~{g.node_count} "
+                                   f"nodes), {args.pair_iters} fixed-count iterations each",
+                       "parallelism": f"pairs round-robin over {dist.world} GPU(s), no communication",
+                       "pairs_per_s": args.pairs / (max_ms / 1e3)},
+            "kernel_ms_per_step": {k: v / max(1, iters) for k, v in (kms or {}).items()},
+            "e2e": {"value": e2e, "unit": UNIT, "seconds": wall, "note": "wall clock incl. per-pair setup"},
+            "gpu_launches": launches, "clocks": clocks.result(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
 def main():
     args = parse()
     dist = Dist()
     if args.impl == "reference":
         run_reference(args, dist)
+    elif args.config == 3:
+        run_pairs(args, dist)
     else:
         run_b200(args, dist)
 

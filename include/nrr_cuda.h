@@ -145,6 +145,18 @@ int nrr_ctx_finish(nrr_ctx* ctx, double* out_X, double* out_deformed);
 int nrr_register(nrr_ctx* ctx, const nrr_problem_view* p, const nrr_solver_config* cfg,
                  double* out_X, double* out_deformed);
 
+/* Vertex-sharded registration over NCCL (config 4): every
+ * rank calls nrr_ctx_set_comm with the same 128-byte id (from
+ * nrr_comm_unique_id on rank 0, broadcast by the caller), then
+ * nrr_ctx_set_shard(n_global) and sets a problem view holding ITS contiguous
+ * slice of the source vertices (influence CSR rebased) with the full target
+ * and graph. The partial energies, K, B and max displacement are allreduced
+ * every pass; the solve and Anderson run replicated. Outputs: X (identical on
+ * all ranks) and the rank's slice of the deformed points. */
+int nrr_comm_unique_id(void* out128);
+int nrr_ctx_set_comm(nrr_ctx* ctx, const void* id128, int32_t nranks, int32_t rank);
+int nrr_ctx_set_shard(nrr_ctx* ctx, int32_t n_global);
+
 /* report of the last run */
 int nrr_ctx_report(nrr_ctx* ctx, nrr_report_summary* summary, nrr_stage_record* stages,
                    int32_t stage_cap, nrr_iteration_record* iters, int32_t iter_cap,

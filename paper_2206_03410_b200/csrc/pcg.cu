@@ -993,10 +993,10 @@ void rcb(RcbCtx& ctx, int lo, int hi, int g0, int g1) {
 void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit) {
     nodes = N;
     grid = std::max(1, std::min({num_sms, N, 32 * kMaxGridLoads}));
-    const int cap_rows = (kPcgThreads * 4) / 12;
+    const int cap_rows = (kPcgThreads * kMaxEpt) / 12;
     while ((N + grid - 1) / grid > cap_rows * 7 / 8 && grid < std::min(num_sms, 32 * kMaxGridLoads)) ++grid;
     if ((N + grid - 1) / grid > cap_rows)
-        throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 170)");
+        throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 256)");
     std::vector<int> ids(N), w(N);
     std::iota(ids.begin(), ids.end(), 0);
     for (int j = 0; j < N; ++j) w[j] = 2 + row_nnz_by_node[j];
@@ -1009,9 +1009,10 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
     for (int r = 0; r < N; ++r) node_row[row_node[r]] = r;
     max_rows = 0;
     for (int g = 0; g < grid; ++g) max_rows = std::max(max_rows, row_begin[g + 1] - row_begin[g]);
-    if (max_rows * 12 > kPcgThreads * 4)
-        throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 170)");
-    ept = max_rows * 12 <= kPcgThreads ? 1 : (max_rows * 12 <= 2 * kPcgThreads ? 2 : 4);
+    if (max_rows * 12 > kPcgThreads * kMaxEpt)
+        throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 256)");
+    ept = 1;
+    while (max_rows * 12 > ept * kPcgThreads) ept *= 2;
     // aggregates: consecutive CTAs, coarse dimension 4 * n_agg <= kCoarseMax (160)
     agg_ctas = std::max(8, (4 * grid + 159) / 160);  // 8 CTAs per aggregate measured best on cfg2
     if (const char* e = std::getenv("NRR_AGG_CTAS")) agg_ctas = std::max((4 * grid + 159) / 160, std::atoi(e));
@@ -1130,7 +1131,8 @@ void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
     void* kargs[] = {&args};
     const void* fn = plan.ept == 1   ? reinterpret_cast<const void*>(pcg_kernel<1>)
                      : plan.ept == 2 ? reinterpret_cast<const void*>(pcg_kernel<2>)
-                                     : reinterpret_cast<const void*>(pcg_kernel<4>);
+                     : plan.ept == 4 ? reinterpret_cast<const void*>(pcg_kernel<4>)
+                                     : reinterpret_cast<const void*>(pcg_kernel<8>);
     NRR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem_bytes)));
     int per_sm = 0;
     NRR_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPcgThreads, plan.smem_bytes));

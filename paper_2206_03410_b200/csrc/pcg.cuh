@@ -10,7 +10,8 @@ namespace nrr_b200 {
 
 constexpr int kPcgThreads = 384;  // multiple of 12: (row r, column c) fixed per thread; 12 warps leave 168 registers
 constexpr int kCoarseMax = 256;
-constexpr int kPcgSlots = 32;   // reduction slots per CTA in part_a / part_b
+constexpr int kPcgSlots = 32;
+constexpr int kMaxEpt = 8;       // elements per thread: up to 256 nodes per CTA   // reduction slots per CTA in part_a / part_b
 constexpr int kSubRowsMax = 16;  // nodes per dense subdomain block (64 scalar rows; measured best on cfg2)
 // leading dimension of a 4s x 4s subdomain inverse: >= 4s and = 4 (mod 16), so
 // the 4 threads x 4 rows of a half-warp hit 16 distinct bank pairs

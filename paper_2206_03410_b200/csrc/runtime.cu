@@ -26,6 +26,7 @@
 #include "nrr_cuda.h"
 #include "pcg.cuh"
 #include "pcg_cluster.cuh"
+#include "comm.hpp"
 
 namespace nrr_b200 {
 
@@ -117,6 +118,10 @@ using namespace nrr_b200;
 struct nrr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // vertex sharding (comm.hpp): this rank's problem view is its vertex
+    // slice; n_global = all ranks' vertices (term weights, median)
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0, n_global = -1;
     cudaStream_t side = nullptr;  // subdomain inverses run beside the coarse setup
     cudaEvent_t fork = nullptr, join = nullptr;
     int num_sms = 0;
@@ -191,6 +196,7 @@ struct nrr_ctx {
                 if (x) cudaEventDestroy(x);
         for (auto& x : pass_ev)
             if (x) cudaEventDestroy(x);
+        if (comm) nrr_b200::nccl().comm_destroy(comm);
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
         if (side) cudaStreamDestroy(side);
@@ -633,6 +639,31 @@ void validate(const nrr_solver_config& cfg) {  // solver.hpp:32-38
     if (cfg.k_alpha < 0.0 || cfg.k_beta < 0.0) throw ConfigError("k_alpha and k_beta must be non-negative");
 }
 
+// ---- vertex sharding collectives (no-ops on an unsharded context)
+int n_total(const nrr_ctx* c) { return c->n_global >= 0 ? c->n_global : c->n; }
+
+void allreduce(nrr_ctx* c, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op) {
+    if (!c->comm) return;
+    nccl_check(nccl().all_reduce(buf, buf, count, t, op, c->comm, c->stream), "allreduce");
+}
+
+// after the terms: the node terms (reg, rot) exist on rank 0 only, then the
+// five energy sums are added over ranks
+void reduce_energies(nrr_ctx* c) {
+    if (!c->comm) return;
+    if (c->rank > 0) NRR_CUDA_CHECK(cudaMemsetAsync(&c->d_rec.p->reg, 0, 2 * sizeof(double), c->stream));
+    allreduce(c, &c->d_rec.p->align, 5, ncclFloat64, ncclSum);
+}
+
+// node-level terms (regularisation, rotation, beta) are assembled on rank 0 only
+TermParams local_terms(const nrr_ctx* c, TermParams tp) {
+    if (c->comm && c->rank > 0) {
+        tp.alpha = 0.0;
+        tp.beta = 0.0;
+    }
+    return tp;
+}
+
 void update_term_weights(Params& p, int n, int E, int N, const nrr_solver_config& cfg) {  // solver.hpp:68-80
     if (E == 0) {
         p.alpha = 0.0;
@@ -649,14 +680,39 @@ Params init_parameters(nrr_ctx* c, const nrr_solver_config& cfg) {  // solver.hp
     const int n = c->n;
     nn_run(c, c->d_src.p, n, nullptr, c->nn_idx.p, c->d2.p, nullptr, nullptr);
     std::vector<double> dist(n);
-    NRR_CUDA_CHECK(cudaMemcpyAsync(dist.data(), c->d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
+    if (c->comm) {  // all ranks' distances: gather padded slices (padding = NaN, dropped)
+        int mx = n;
+        DevBuf<int> dm;
+        dm.upload(&mx, 1, c->stream);
+        allreduce(c, dm.p, 1, ncclInt32, ncclMax);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(&mx, dm.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+        DevBuf<double> pad, all;
+        pad.resize(std::max(mx, 1));
+        const double qnan = std::numeric_limits<double>::quiet_NaN();
+        std::vector<double> hpad(std::max(mx, 1), qnan);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(pad.p, hpad.data(), sizeof(double) * hpad.size(), cudaMemcpyHostToDevice, c->stream));
+        NRR_CUDA_CHECK(cudaMemcpyAsync(pad.p, c->d2.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+        all.resize(static_cast<size_t>(std::max(mx, 1)) * c->nranks);
+        nccl_check(nccl().all_gather(pad.p, all.p, std::max(mx, 1), ncclFloat64, c->comm, c->stream), "allgather");
+        std::vector<double> h(all.n);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(h.data(), all.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+        dist.clear();
+        for (double v : h)
+            if (!std::isnan(v)) dist.push_back(v);
+        if (static_cast<int>(dist.size()) != n_total(c)) throw ConfigError("sharded vertex counts do not add up");
+    } else {
+        NRR_CUDA_CHECK(cudaMemcpyAsync(dist.data(), c->d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+    }
     for (auto& d : dist) d = std::sqrt(d);
+    const int n_med = static_cast<int>(dist.size());
     double median = 0.0;
-    if (n > 0) {  // the sorted-order median (solver.hpp:92-100) by selection
-        std::nth_element(dist.begin(), dist.begin() + n / 2, dist.end());
-        const double hi = dist[n / 2];
-        median = n % 2 == 1 ? hi : 0.5 * (*std::max_element(dist.begin(), dist.begin() + n / 2) + hi);
+    if (n_med > 0) {  // the sorted-order median (solver.hpp:92-100) by selection
+        std::nth_element(dist.begin(), dist.begin() + n_med / 2, dist.end());
+        const double hi = dist[n_med / 2];
+        median = n_med % 2 == 1 ? hi : 0.5 * (*std::max_element(dist.begin(), dist.begin() + n_med / 2) + hi);
     }
     Params p;
     const double l_bar = c->src_avg;
@@ -664,7 +720,7 @@ Params init_parameters(nrr_ctx* c, const nrr_solver_config& cfg) {  // solver.hp
     p.nu_a = std::isnan(cfg.nu_a_init) ? std::max(median, p.nu_a_min) : cfg.nu_a_init;
     p.nu_r = std::isnan(cfg.nu_r_init) ? 3.0 * l_bar : cfg.nu_r_init;
     if (!(p.nu_a > 0.0) || !(p.nu_r > 0.0)) throw NumericalError("init_parameters: Welsch parameters must be positive");
-    update_term_weights(p, n, c->E, c->N, cfg);
+    update_term_weights(p, n_total(c), c->E, c->N, cfg);
     return p;
 }
 
@@ -827,6 +883,7 @@ void run_begin(nrr_ctx* c, const nrr_solver_config& cfg_in) {
     c->iters.clear();
     c->passes.clear();
     c->pass_nn.clear();
+    if (c->comm && r.cfg.landmark_count > 0) throw ConfigError("landmarks are not supported on a vertex-sharded run");
     upload_landmarks(c, r.cfg);
     r.prm = init_parameters(c, r.cfg);
     ensure_aa(c, r.cfg.aa_window, 12 * c->N);
@@ -863,7 +920,7 @@ void close_stage(nrr_ctx* c) {
     }
     r.prm.nu_a = std::max(r.prm.nu_a / 2.0, r.prm.nu_a_min);
     r.prm.nu_r = std::max(r.prm.nu_r / 2.0, r.cfg.nu_r_floor);
-    update_term_weights(r.prm, c->n, c->E, c->N, r.cfg);
+    update_term_weights(r.prm, n_total(c), c->E, c->N, r.cfg);
 }
 
 // One evaluated pass (solver.hpp:225-288). Returns true when an iteration was
@@ -873,12 +930,13 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     const int N = c->N, n = c->n, D = 12 * N;
     *stage_end = false;
     if (++r.passes > 2 * r.cfg.i_max + 4) throw NumericalError("solver stage failed to make progress");
-    const TermParams tp{r.prm.alpha, r.prm.beta, r.prm.nu_a, r.prm.nu_r, r.lm_w};
+    const TermParams tp = local_terms(c, TermParams{r.prm.alpha, r.prm.beta, r.prm.nu_a, r.prm.nu_r, r.lm_w});
     bool ran[nrr_ctx::kClasses];
     std::fill(ran, ran + nrr_ctx::kClasses, false);
     NRR_CUDA_CHECK(cudaMemsetAsync(c->d_rec.p, 0, sizeof(PassRecord), c->stream));
     // warm start from the previous pass's correspondences (init NN at the first pass)
     evaluate(c, c->x.p, c->vhat.p, tp, true);
+    reduce_energies(c);
     ran[kNN] = ran[kTerms] = true;
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_deg.p, c->deg.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -905,7 +963,12 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     r.e_prev = e_accept;
     nrr_iteration_record rec{e.total, e.align, e.reg, e.rot, e.landmark, 0.0, r.current_is_aa ? 1 : 0, r.si};
     std::fill(ran, ran + nrr_ctx::kClasses, false);
-    assemble_solve(c, tp, c->x.p, c->xmm.p);  // x_mm = solve(), warm start at x
+    assemble(c, tp);
+    if (c->comm) {  // the replicated solve needs the full K and B (north_star: allreduce before the solve)
+        allreduce(c, c->K.p, 16 * static_cast<size_t>(c->dp.nnzb), ncclFloat64, ncclSum);
+        allreduce(c, c->B.p, 12 * static_cast<size_t>(N), ncclFloat64, ncclSum);
+    }
+    solve(c, c->x.p, c->xmm.p);  // x_mm = solve(), warm start at x
     ran[kAsm] = ran[kPcg] = true;
     aa_push_combine(c, r.win, c->xmm.p, c->x.p, nullptr, c->xnext.p, D);
     ran[kAA] = true;
@@ -913,6 +976,8 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     NRR_CUDA_CHECK(cudaMemsetAsync(&c->d_rec.p->max_disp, 0, sizeof(double), c->stream));
     deform_run(c, c->xnext.p, c->vhat2.p, c->vhat.p, &c->d_rec.p->max_disp);
     ran[kDeform] = true;
+    allreduce(c, &c->d_rec.p->max_disp, 1, ncclFloat64, ncclMax);
+    allreduce(c, &c->d_rec.p->nonfinite, 1, ncclInt32, ncclMax);
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_status.p, c->d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
@@ -1055,6 +1120,37 @@ int nrr_ctx_set_options(nrr_ctx* ctx, const nrr_solve_options* opt) {
 int nrr_ctx_enable_timing(nrr_ctx* ctx, int32_t on) {
     ctx->timing = on != 0;
     return 0;
+}
+
+int nrr_comm_unique_id(void* out128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        nccl_check(nccl().get_unique_id(&id), "get unique id");
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+int nrr_ctx_set_comm(nrr_ctx* ctx, const void* id128, int32_t nranks, int32_t rank) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw ConfigError("set_comm: bad rank / size");
+        if (ctx->comm) {
+            nccl().comm_destroy(ctx->comm);
+            ctx->comm = nullptr;
+        }
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        nccl_check(nccl().comm_init_rank(&ctx->comm, nranks, id, rank), "comm init");
+    });
+}
+
+int nrr_ctx_set_shard(nrr_ctx* ctx, int32_t n_global) {
+    return guarded([&] {
+        if (n_global < -1) throw ConfigError("set_shard: bad vertex count");
+        ctx->n_global = n_global;
+    });
 }
 
 int nrr_ctx_set_target(nrr_ctx* ctx, const double* target, int32_t m) {

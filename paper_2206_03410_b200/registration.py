@@ -177,6 +177,31 @@ def synth(config, seed=None, scale=1.0):
     return src, (faces if nf.value else None), tgt
 
 
+def shard_bounds(n, world, rank):
+    """Contiguous vertex slice [v0, v1) of `rank`."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def shard_problem(p: Problem, v0, v1) -> Problem:
+    """The problem view of one vertex shard: source slice with its influence
+    CSR rebased; the target and the deformation graph stay whole (replicated)."""
+    g = p.graph
+    off = np.asarray(g.infl_offsets)
+    k0, k1 = int(off[v0]), int(off[v1])
+    g2 = Graph(g.node_indices, g.node_positions, g.edges, (off[v0:v1 + 1] - k0).astype(np.int32),
+               g.infl_nodes[k0:k1], g.infl_weights[k0:k1], g.infl_dist[k0:k1], g.reg_pairs, g.reg_weights,
+               g.radius)
+    return Problem(p.source[v0:v1], p.target, g2, p.src_avg_edge_length, None)
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id for Context.set_comm (call on rank 0, broadcast the bytes)."""
+    lib = capi.load()
+    buf = (C.c_char * 128)()
+    check(lib.nrr_comm_unique_id(buf))
+    return bytes(buf)
+
+
 def make_problem(config, seed=None, scale=1.0, mult=None):
     """Synthetic pair -> normalize -> connectivity -> reference graph."""
     src, faces, tgt = synth(config, seed, scale)
@@ -237,6 +262,15 @@ class Context:
     def set_options(self, pcg_rtol=1e-13, pcg_max_iter=20000, record_passes=0):
         o = capi.SolveOptions(pcg_rtol, pcg_max_iter, record_passes)
         check(self.lib.nrr_ctx_set_options(self.h, C.byref(o)))
+
+    def set_comm(self, unique_id: bytes, world: int, rank: int):
+        """Join the vertex-sharded run (NCCL communicator of this context)."""
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        check(self.lib.nrr_ctx_set_comm(self.h, buf, world, rank))
+
+    def set_shard(self, n_global: int):
+        """This context's problem view is one vertex slice of n_global vertices."""
+        check(self.lib.nrr_ctx_set_shard(self.h, n_global))
 
     def enable_timing(self, on=True):
         self.lib.nrr_ctx_enable_timing(self.h, 1 if on else 0)

@@ -1,0 +1,135 @@
+"""Vertex sharding of one registration (config 4).
+
+CPU (gloo, world size 2): the decomposition the device path relies on --
+each rank assembles the alignment part of K, B and the energy from its vertex
+slice (shard_problem), rank 0 adds the node terms, and the allreduced sums
+equal the unsharded system -- checked with the oracle as the per-rank
+assembler; the median of the gathered slice distances gives the global nu_a
+(init_parameters, solver.hpp:86-106).
+
+GPU (one device): the NCCL path with a one-rank communicator reproduces the
+unsharded run exactly (the collectives and the rank-0 node terms are on the
+path; several ranks need several GPUs, which the round-end box does not
+have)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2206_03410_b200 import registration as R
+from tests.helpers import random_transforms, strip_problem
+
+
+def test_shard_bounds_partition():
+    for n in (1, 7, 100, 99856):
+        for world in (1, 2, 3, 8):
+            if world > n:
+                continue
+            parts = [R.shard_bounds(n, world, r) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            assert all(v1 > v0 for v0, v1 in parts)
+
+
+def test_shard_problem_slices_influence():
+    p = strip_problem(16, 8, seed=3)
+    q = R.shard_problem(p, 40, 90)
+    g, h = p.graph, q.graph
+    assert q.n == 50 and h.infl_offsets[0] == 0
+    for i in range(50):
+        a0, a1 = g.infl_offsets[40 + i], g.infl_offsets[41 + i]
+        b0, b1 = h.infl_offsets[i], h.infl_offsets[i + 1]
+        assert np.array_equal(g.infl_nodes[a0:a1], h.infl_nodes[b0:b1])
+        assert np.array_equal(g.infl_weights[a0:a1], h.infl_weights[b0:b1])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import binding as O
+
+        p = strip_problem(18, 9, seed=11)
+        N = p.graph.node_count
+        nnzb = len(R.bsr_pattern(p.graph)[1])
+        X = random_transforms(N, seed=5, scale=0.05)
+        prm0 = O.init_parameters(p)
+        prm = np.array([prm0["alpha"], prm0["beta"], prm0["nu_a"], prm0["nu_r"]])
+        v0, v1 = R.shard_bounds(p.n, world, rank)
+        q = R.shard_problem(p, v0, v1)
+        local = prm.copy()
+        if rank > 0:  # node terms on rank 0 only
+            local[0] = local[1] = 0.0
+        s = O.step(q, X, local, nnzb, want_solve=False)
+        e = s["energy"].copy()  # align, reg, rot, total
+        if rank > 0:
+            e[1] = e[2] = 0.0
+        K, B, E = (torch.from_numpy(np.ascontiguousarray(a)) for a in (s["K"], s["B"], e))
+        for t in (K, B, E):
+            dist.all_reduce(t)
+        # global median from the gathered slice distances at the identity
+        d = np.sqrt(O.step(q, R.identity_transforms(N), prm, nnzb, want_solve=False)["sqdist"])
+        parts = [None] * world
+        dist.all_gather_object(parts, d)
+        if rank == 0:
+            full = O.step(p, X, prm, nnzb, want_solve=False)
+            kmax = np.max(np.abs(full["K"]))
+            out.put({
+                "K": float(np.max(np.abs(K.numpy() - full["K"])) / kmax),
+                "B": float(np.max(np.abs(B.numpy() - full["B"])) / max(1.0, np.max(np.abs(full["B"])))),
+                "E": float(np.max(np.abs(E.numpy() - full["energy"]) / np.abs(full["energy"]))),
+                "nu_a_gathered": float(max(np.median(np.concatenate(parts)), prm0["nu_a_min"])),
+                "nu_a": float(prm0["nu_a"]),
+            })
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_assembly_allreduce_equals_full():
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.SimpleQueue()
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    res = out.get()
+    assert res["K"] <= 1e-13, res
+    assert res["B"] <= 1e-13, res
+    assert res["E"] <= 1e-12, res
+    assert res["nu_a_gathered"] == res["nu_a"], res
+
+
+@pytest.mark.gpu
+def test_one_rank_nccl_path_matches_unsharded():
+    p = R.make_problem(0, scale=0.4)
+    ref = R.Context()
+    ref.set_problem(p)
+    prm = ref.init_parameters()
+    kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300, i_max=20)
+    X0, v0, r0 = ref.register(R.solver_config(**kw), one_shot_problem=p)
+    Xb, vb, rb = ref.register(R.solver_config(aa_window=0), one_shot_problem=p)
+    ref.close()
+    c = R.Context()
+    try:
+        c.set_comm(R.comm_unique_id(), 1, 0)
+        c.set_shard(p.n)
+        X1, v1, r1 = c.register(R.solver_config(**kw), one_shot_problem=R.shard_problem(p, 0, p.n))
+        e0 = [it["E"] for st in r0["stages"] for it in st["iterations"]]
+        e1 = [it["E"] for st in r1["stages"] for it in st["iterations"]]
+        assert e0 == e1
+        assert np.array_equal(X0, X1) and np.array_equal(v0, v1)
+        # default schedule: nu_a from the median of the gathered distances
+        Xa, va, ra = c.register(R.solver_config(aa_window=0), one_shot_problem=R.shard_problem(p, 0, p.n))
+        assert ra["stages"][0]["nu_a"] == rb["stages"][0]["nu_a"]
+        assert np.array_equal(Xa, Xb)
+    finally:
+        c.close()
