@@ -352,9 +352,12 @@ struct Tri {
             const double ak = a[k];
             if (ak == 0.0) continue;
             const double rk = r[at(k, k)];
-            const double h = sqrt(rk * rk + ak * ak);
-            const double c = rk / h, s = ak / h;
-            r[at(k, k)] = h;
+            // one reciprocal square root instead of sqrt + two divisions
+            // (the merge chains are latency-bound)
+            const double h2 = fma(rk, rk, ak * ak);
+            const double inv = rsqrt(h2);
+            const double c = rk * inv, s = ak * inv;
+            r[at(k, k)] = h2 * inv;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
                 if (j <= k) continue;
@@ -395,22 +398,26 @@ __global__ void __launch_bounds__(kTermThreads) aa_tsqr_kernel(AADevice aa, int 
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) R.shfl_merge(off);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (lane == 0)
 #pragma unroll
         for (int t = 0; t < K * (K + 1) / 2; ++t) sR[w][t] = R.r[t];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) {
+    // fixed binary tree over the warp factors (log2(nw) merges on the critical path)
+    for (int step = 1; step < nw; step <<= 1) {
+        if (lane == 0 && (w & (2 * step - 1)) == 0 && w + step < nw) {
             Tri<K> o;
 #pragma unroll
-            for (int t = 0; t < K * (K + 1) / 2; ++t) o.r[t] = sR[ww][t];
+            for (int t = 0; t < K * (K + 1) / 2; ++t) o.r[t] = sR[w + step][t];
             R.merge(o);
-        }
 #pragma unroll
-        for (int t = 0; t < K * (K + 1) / 2; ++t)
-            aa.partials[static_cast<size_t>(blockIdx.x) * kTriMax + t] = R.r[t];
+            for (int t = 0; t < K * (K + 1) / 2; ++t) sR[w][t] = R.r[t];
+        }
+        __syncthreads();
     }
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int t = 0; t < K * (K + 1) / 2; ++t) aa.partials[static_cast<size_t>(blockIdx.x) * kTriMax + t] = R.r[t];
 }
 
 // Merge the CTA partials (one warp, fixed tree) and finish with the
@@ -423,7 +430,7 @@ __global__ void aa_solve_kernel(AADevice aa, double D, int nblocks) {
     constexpr int mk = K - 1;
     Tri<K> R;
     R.zero();
-    for (int b = threadIdx.x; b < nblocks; b += 32) {
+    for (int b = threadIdx.x; b < nblocks; b += 32) {  // nblocks <= 32: one load per lane
         Tri<K> o;
 #pragma unroll
         for (int t = 0; t < K * (K + 1) / 2; ++t) o.r[t] = aa.partials[static_cast<size_t>(b) * kTriMax + t];
@@ -647,8 +654,11 @@ void launch_aa_update(const AADevice& aa, const double* g, const double* x, cons
 
 template <int K>
 static void aa_solve_k(const AADevice& aa, int D, const SlotList& cols, cudaStream_t s) {
-    aa_tsqr_kernel<K><<<kTermBlocks, kTermThreads, 0, s>>>(aa, D, cols);
-    aa_solve_kernel<K><<<1, 32, 0, s>>>(aa, static_cast<double>(D), kTermBlocks);
+    // 32 CTAs x 256 threads: a few rows per thread, then log-depth merges
+    // (warp shuffles, CTA tree, one warp over the 32 CTA factors)
+    constexpr int kBlocks = 32;
+    aa_tsqr_kernel<K><<<kBlocks, kTermThreads, 0, s>>>(aa, D, cols);
+    aa_solve_kernel<K><<<1, 32, 0, s>>>(aa, static_cast<double>(D), kBlocks);
 }
 
 void launch_aa_solve(const AADevice& aa, int D, const SlotList& cols, cudaStream_t s) {
