@@ -669,63 +669,81 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) vals[base + m * 3 + c] = c == my_c ? ps[m] : 0.0;
     };
-    // z = M_jj r + Psi y_own; y_own = K0inv[own rows] rho (warps 0..11)
+    // z = M_sub r + Psi y_own with y_own = K0inv[own aggregate rows] rho: the
+    // last warp computes y while the others apply the subdomain inverses
     auto precond = [&]() {
-        if (a.use_coarse && (threadIdx.x >> 5) < 12) {
-            const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-            const int k = w / 3, c = w % 3;
-            double sum = 0.0;
-            const double* row = sh.cinv + k * nc;
-            for (int j = lane; j < nc; j += 32) sum += row[j] * sh.rho[j * 3 + c];
-            sum = warp_sum(sum);
-            if (lane == 0) sh.y[k * 3 + c] = sum;
-        }
 #pragma unroll
         for (int k = 0; k < EPT; ++k)
             if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = rr[k];
         __syncthreads();
-        // zz = M_sub r: 4 threads per scalar row i split the chunk's columns,
-        // butterfly-combined in a fixed order
-        for (int t = threadIdx.x; t < 16 * nrows; t += blockDim.x) {
-            const int i = t >> 2, q = t & 3, lr = i >> 2;
-            const int ch = sh.rchunk[lr], st = sh.cstart[ch];
-            const int nk = 4 * (sh.cstart[ch + 1] - st);
-            const double* m = sh.Minv + ch * sub_msz + static_cast<size_t>(i - 4 * st) * sub_ld;
-            const double* rv = sh.rex + 12 * st;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
-            int j = q;
-            for (; j + 4 < nk; j += 8) {
-                const double mj = m[j], mk = m[j + 4];
-                a0 = fma(mj, rv[3 * j], a0);
-                b0 = fma(mk, rv[3 * j + 12], b0);
-                a1 = fma(mj, rv[3 * j + 1], a1);
-                b1 = fma(mk, rv[3 * j + 13], b1);
-                a2 = fma(mj, rv[3 * j + 2], a2);
-                b2 = fma(mk, rv[3 * j + 14], b2);
+        const int wlast = (blockDim.x >> 5) - 1;
+        if (a.use_coarse && (threadIdx.x >> 5) == wlast) {
+            const int lane = threadIdx.x & 31;
+            double acc[12];
+#pragma unroll
+            for (int o = 0; o < 12; ++o) acc[o] = 0.0;
+            for (int j = lane; j < nc; j += 32) {
+                const double r0 = sh.rho[j * 3], r1 = sh.rho[j * 3 + 1], r2 = sh.rho[j * 3 + 2];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double ci = sh.cinv[k * nc + j];
+                    acc[3 * k] += ci * r0;
+                    acc[3 * k + 1] += ci * r1;
+                    acc[3 * k + 2] += ci * r2;
+                }
             }
-            if (j < nk) {
-                const double mj = m[j];
-                a0 = fma(mj, rv[3 * j], a0);
-                a1 = fma(mj, rv[3 * j + 1], a1);
-                a2 = fma(mj, rv[3 * j + 2], a2);
-            }
-            a0 += b0;
-            a1 += b1;
-            a2 += b2;
-            const unsigned grp = 0xFu << (threadIdx.x & 28);
-            a0 += __shfl_xor_sync(grp, a0, 1);
-            a1 += __shfl_xor_sync(grp, a1, 1);
-            a2 += __shfl_xor_sync(grp, a2, 1);
-            a0 += __shfl_xor_sync(grp, a0, 2);
-            a1 += __shfl_xor_sync(grp, a1, 2);
-            a2 += __shfl_xor_sync(grp, a2, 2);
-            if (q == 0) {
-                sh.zz[3 * i] = a0;
-                sh.zz[3 * i + 1] = a1;
-                sh.zz[3 * i + 2] = a2;
+#pragma unroll
+            for (int o = 0; o < 12; ++o) acc[o] = warp_sum(acc[o]);
+            if (lane == 0)
+#pragma unroll
+                for (int o = 0; o < 12; ++o) sh.y[o] = acc[o];
+        } else {
+            // zz = M_sub r: 4 threads per scalar row i split the chunk's
+            // columns, butterfly-combined in a fixed order
+            const int nthr = a.use_coarse ? wlast * 32 : static_cast<int>(blockDim.x);
+            for (int t = threadIdx.x; t < 16 * nrows; t += nthr) {
+                const int i = t >> 2, q = t & 3, lr = i >> 2;
+                const int ch = sh.rchunk[lr], st = sh.cstart[ch];
+                const int nk = 4 * (sh.cstart[ch + 1] - st);
+                const double* m = sh.Minv + ch * sub_msz + static_cast<size_t>(i - 4 * st) * sub_ld;
+                const double* rv = sh.rex + 12 * st;
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+                int j = q;
+                for (; j + 4 < nk; j += 8) {
+                    const double mj = m[j], mk = m[j + 4];
+                    a0 = fma(mj, rv[3 * j], a0);
+                    b0 = fma(mk, rv[3 * j + 12], b0);
+                    a1 = fma(mj, rv[3 * j + 1], a1);
+                    b1 = fma(mk, rv[3 * j + 13], b1);
+                    a2 = fma(mj, rv[3 * j + 2], a2);
+                    b2 = fma(mk, rv[3 * j + 14], b2);
+                }
+                if (j < nk) {
+                    const double mj = m[j];
+                    a0 = fma(mj, rv[3 * j], a0);
+                    a1 = fma(mj, rv[3 * j + 1], a1);
+                    a2 = fma(mj, rv[3 * j + 2], a2);
+                }
+                a0 += b0;
+                a1 += b1;
+                a2 += b2;
+                const unsigned grp = 0xFu << (threadIdx.x & 28);
+                a0 += __shfl_xor_sync(grp, a0, 1);
+                a1 += __shfl_xor_sync(grp, a1, 1);
+                a2 += __shfl_xor_sync(grp, a2, 1);
+                a0 += __shfl_xor_sync(grp, a0, 2);
+                a1 += __shfl_xor_sync(grp, a1, 2);
+                a2 += __shfl_xor_sync(grp, a2, 2);
+                if (q == 0) {
+                    sh.zz[3 * i] = a0;
+                    sh.zz[3 * i + 1] = a1;
+                    sh.zz[3 * i + 2] = a2;
+                }
             }
         }
         __syncthreads();
+        // z = zz + Psi y; own rows of the SpMV operand (ext) are written here:
+        // ext is next read after the halo barrier
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
             if (el_row[k] < 0) {
@@ -742,11 +760,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             }
             zr[k] = z;
             __stcg(a.Z + el_g[k], z);
+            sh.ext[lr * 12 + my_rc] = z;
         }
-        __syncthreads();  // all rex reads done before own z overwrites ext
-#pragma unroll
-        for (int k = 0; k < EPT; ++k)
-            if (el_row[k] >= 0) sh.ext[el_row[k] * 12 + my_rc] = zr[k];
     };
 
     probe(13);  // Gauss-Jordan
@@ -780,6 +795,15 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             acc_t[slot] += t - tp;
             tp = t;
         }
+    };
+    // per-CTA work (not waiting) cycles: spmv+partials, update+precond, halo
+    const bool cprof = a.cta_prof != nullptr && threadIdx.x == 0;
+    long long cw[3] = {0, 0, 0}, ct = 0;
+    auto cstart_t = [&]() {
+        if (cprof) ct = clock64();
+    };
+    auto cstop_t = [&](int k) {
+        if (cprof) cw[k] += clock64() - ct;
     };
 
     while (true) {
@@ -841,6 +865,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             fill_halo(a.Z);
         }
         mark(7);
+        cstart_t();
         // ---- w = K u; partials (r,u), (w,u), max|r|, Psi^T w
         {
             double g = 0.0, dl = 0.0, rmx = 0.0, ps[4] = {0, 0, 0, 0};
@@ -860,6 +885,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             vals[6] = rmx;
             if (a.use_coarse) put_psi(7, ps);
         }
+        cstop_t(0);
         mark(0);
         block_partials(vals, a.use_coarse ? 19 : 7, sh.red, a.part_a, 1u << 6);
         mark(1);
@@ -907,6 +933,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                 sh.sig[o] = sg;
                 sh.rho[o] -= al[o % 3] * sg;
             }
+        cstart_t();
         // ---- p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = M r
         {
             const double a_c = al[my_c], b_c = bt[my_c];
@@ -921,13 +948,16 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         }
         __syncthreads();  // rho updated before the coarse solve
         precond();
+        cstop_t(1);
         mark(4);
         ++it;
         // u of the neighbours visible (a neighbour-only flag barrier was
         // measured slower: the skew then piles up at the reduction barrier)
         grid.sync();
         mark(5);
+        cstart_t();
         fill_halo(a.Z);
+        cstop_t(2);
         mark(6);
     }
 #pragma unroll
@@ -939,6 +969,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         a.prof[8] += t_setup;
         a.prof[9] += 1;
     }
+    if (cprof)
+        for (int k = 0; k < 3; ++k) a.cta_prof[cta * 4 + k] += cw[k];
     if (cta == 0 && threadIdx.x == 0) {
         a.status->iterations = it;
         a.status->code = status_code;

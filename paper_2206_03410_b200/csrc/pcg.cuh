@@ -60,6 +60,7 @@ struct PcgArgs {
     int sub_rows, sub_ld, sub_chunks;  // subdomain block-Jacobi plan
     int agg_ctas, n_agg, use_coarse;
     long long* prof;  // optional clock64 per phase (CTA 0), accumulated
+    long long* cta_prof;  // optional per-CTA work cycles [grid][4] (NRR_PROF)
 };
 
 struct PcgPlan {

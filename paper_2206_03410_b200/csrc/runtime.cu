@@ -160,7 +160,7 @@ struct nrr_ctx {
     bool use_cluster = false;
     DevBuf<int> c_rank_rows, c_row_node, c_ent_ptr, c_diag_ent, c_store_off, c_store_src, c_halo_off;
     DevBuf<int2> c_ent, c_halo_src;
-    DevBuf<long long> prof;
+    DevBuf<long long> prof, cta_prof;
     DevBuf<PcgStatus> d_status;
     DevBuf<PassRecord> d_rec;
     Pinned<PassRecord> h_rec;
@@ -831,6 +831,11 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
             c->prof.zero(c->stream);
         }
         a.prof = c->prof.p;
+        if (c->cta_prof.n == 0) {
+            c->cta_prof.resize(4 * static_cast<size_t>(c->plan.grid));
+            c->cta_prof.zero(c->stream);
+        }
+        a.cta_prof = c->cta_prof.p;
     }
     // the subdomain inverses and the coarse operator both depend on K only:
     // run them side by side (one CTA per SM for the former, one CTA for the
@@ -1545,6 +1550,21 @@ int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* 
         std::fprintf(stderr, "pcg phase cycles: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
                      h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
         std::fprintf(stderr, "pcg setup cycles: %lld %lld %lld %lld %lld %lld\n", h[10], h[11], h[12], h[13], h[14], h[15]);
+        if (ctx->cta_prof.n) {
+            std::vector<long long> cp(ctx->cta_prof.n);
+            cudaMemcpy(cp.data(), ctx->cta_prof.p, sizeof(long long) * cp.size(), cudaMemcpyDeviceToHost);
+            const int G = static_cast<int>(cp.size() / 4);
+            for (int k = 0; k < 3; ++k) {
+                long long mx = 0, sum = 0;
+                int arg = 0;
+                for (int g = 0; g < G; ++g) {
+                    sum += cp[4 * g + k];
+                    if (cp[4 * g + k] > mx) mx = cp[4 * g + k], arg = g;
+                }
+                std::fprintf(stderr, "cta work %d: mean %lld max %lld (cta %d, rows %d)\n", k, sum / G, mx, arg,
+                             ctx->plan.row_begin[arg + 1] - ctx->plan.row_begin[arg]);
+            }
+        }
     }
     if (launches) *launches = ctx->launches;
     if (kernel_ms6)
