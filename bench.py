@@ -314,6 +314,7 @@ def run_b200(args, dist):
         except Exception:
             traffic = None
 
+    ctx.close()  # the one-shot call below creates its own context, as a user would
     # end-to-end through the C ABI with host buffers (uploads, index build,
     # init_parameters, K iterations, downloads), wall clock around the call
     e2e_ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
@@ -335,7 +336,6 @@ def run_b200(args, dist):
         cpu = {"value": cps, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"{args.cpu_steps} MM iterations of config {args.config} (n={n}) after 1 warm-up, "
                          "oracle restatement, one thread (the reference is single-threaded)"}
-    ctx.close()
     if dist.rank == 0:
         line = {
             "metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": K,

@@ -17,6 +17,9 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <unordered_map>
+#include <mutex>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -35,6 +38,56 @@ thread_local std::string g_last_error;
 }
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+// Process-wide cache of device blocks (per device, by size): contexts are
+// created per registration, and cudaMalloc / cudaFree of their ~50 buffers
+// (mapping and synchronising) cost more than the setup itself. Blocks return
+// to the cache when a buffer is released; every C-ABI call synchronises its
+// stream before returning and a context synchronises before it is destroyed,
+// so a cached block is never handed out while queued work still uses it.
+class BlockCache {
+public:
+    void* get(size_t bytes) {
+        int dev = 0;
+        NRR_CUDA_CHECK(cudaGetDevice(&dev));
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto& m = free_[dev];
+            auto it = m.lower_bound(bytes);
+            if (it != m.end() && it->first <= 2 * bytes + (1 << 20)) {
+                void* ptr = it->second;
+                sizes_[ptr] = it->first;
+                m.erase(it);
+                return ptr;
+            }
+        }
+        void* ptr = nullptr;
+        const size_t rounded = (bytes + 511) & ~static_cast<size_t>(511);
+        NRR_CUDA_CHECK(cudaMalloc(&ptr, rounded));
+        std::lock_guard<std::mutex> lk(mu_);
+        sizes_[ptr] = rounded;
+        devs_[ptr] = dev;
+        return ptr;
+    }
+    void put(void* ptr) {
+        std::lock_guard<std::mutex> lk(mu_);
+        free_[devs_[ptr]].emplace(sizes_[ptr], ptr);
+    }
+    size_t capacity(void* ptr) {
+        std::lock_guard<std::mutex> lk(mu_);
+        return sizes_[ptr];
+    }
+
+private:
+    std::mutex mu_;
+    std::map<int, std::multimap<size_t, void*>> free_;
+    std::unordered_map<void*, size_t> sizes_;
+    std::unordered_map<void*, int> devs_;
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache();  // never destroyed: blocks live until process exit
+    return *c;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -44,7 +97,7 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) block_cache().put(p);
         p = nullptr;
         n = cap = 0;
     }
@@ -55,8 +108,9 @@ struct DevBuf {
         }
         release();
         if (count == 0) return;
-        NRR_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
-        n = cap = count;
+        p = static_cast<T*>(block_cache().get(count * sizeof(T)));
+        n = count;
+        cap = block_cache().capacity(p) / sizeof(T);
     }
     void upload(const T* h, size_t count, cudaStream_t s) {
         resize(count);
@@ -1113,7 +1167,13 @@ int nrr_ctx_create(int device, nrr_ctx** out) {
     });
 }
 
-void nrr_ctx_destroy(nrr_ctx* ctx) { delete ctx; }
+void nrr_ctx_destroy(nrr_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);  // buffers go back to the block cache
+    if (ctx->side) cudaStreamSynchronize(ctx->side);
+    delete ctx;
+}
 
 int nrr_ctx_set_options(nrr_ctx* ctx, const nrr_solve_options* opt) {
     return guarded([&] {
