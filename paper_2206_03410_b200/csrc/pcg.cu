@@ -602,9 +602,24 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     // stage the halo rows of v (global, written by other CTAs before the last
     // grid barrier) into shared memory next to the own rows: one coalesced
     // round of L2 loads instead of a latency-bound gather per K block
+    // the thread's first kHaloRegs halo elements: global offsets resolved once,
+    // so a fill is kHaloRegs independent L2 loads (one round trip)
+    constexpr int kHaloRegs = 4;
+    int hoff[kHaloRegs];
+#pragma unroll
+    for (int k = 0; k < kHaloRegs; ++k) {
+        const int t = nrows * 12 + threadIdx.x + k * blockDim.x;
+        hoff[k] = t < n_ext * 12 ? a.ext_node[e0 + t / 12] * 12 + t % 12 : -1;
+    }
     auto fill_halo = [&](const double* __restrict__ v) {
-        for (int t = nrows * 12 + threadIdx.x; t < n_ext * 12; t += blockDim.x)
+        double hv[kHaloRegs];
+#pragma unroll
+        for (int k = 0; k < kHaloRegs; ++k) hv[k] = hoff[k] >= 0 ? __ldcg(v + hoff[k]) : 0.0;
+        for (int t = nrows * 12 + threadIdx.x + kHaloRegs * blockDim.x; t < n_ext * 12; t += blockDim.x)
             sh.ext[t] = __ldcg(v + static_cast<size_t>(a.ext_node[e0 + t / 12]) * 12 + t % 12);
+#pragma unroll
+        for (int k = 0; k < kHaloRegs; ++k)
+            if (hoff[k] >= 0) sh.ext[nrows * 12 + threadIdx.x + k * blockDim.x] = hv[k];
         __syncthreads();
     };
     auto spmv = [&](int k) -> double {
@@ -1031,7 +1046,9 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
         throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 256)");
     std::vector<int> ids(N), w(N);
     std::iota(ids.begin(), ids.end(), 0);
-    for (int j = 0; j < N; ++j) w[j] = 2 + row_nnz_by_node[j];
+    int wbase = 6;  // RCB cost per node: wbase + its block count (6 measured best on cfg2)
+    if (const char* e = std::getenv("NRR_RCB_W")) wbase = std::atoi(e);
+    for (int j = 0; j < N; ++j) w[j] = wbase + row_nnz_by_node[j];
     row_begin.assign(grid + 1, N);
     RcbCtx ctx{node_pos, w.data(), &ids, &row_begin};
     rcb(ctx, 0, N, 0, grid);

@@ -10,6 +10,7 @@
 // the solve status; all vectors stay resident in HBM.
 #include <algorithm>
 #include <chrono>
+#include <exception>
 #include <thread>
 #include <cmath>
 #include <cstdlib>
@@ -299,9 +300,9 @@ void nn_run(nrr_ctx* c, const double* queries, int nq, const int* prev, int* idx
     ++c->launches;
 }
 
-void set_target(nrr_ctx* c, const double* tgt, int m) {
+void set_target(nrr_ctx* c, const double* tgt, int m, bool built = false) {
     if (m <= 0) throw NumericalError("SpatialIndex: cannot index an empty point set");
-    c->bvh.build(tgt, m);
+    if (!built) c->bvh.build(tgt, m);
     c->d_tgt.upload(tgt, static_cast<size_t>(m) * 3, c->stream);
     c->d_pts.upload(c->bvh.pts.data(), c->bvh.pts.size(), c->stream);
     c->d_lo.upload(c->bvh.box_lo.data(), c->bvh.box_lo.size(), c->stream);
@@ -1273,8 +1274,26 @@ int nrr_register(nrr_ctx* ctx, const nrr_problem_view* p, const nrr_solver_confi
         NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
         validate(*cfg);
         if (p->n == 0 || p->m == 0) throw NumericalError("register_surfaces: empty surface");
-        set_target(ctx, p->target, p->m);
-        set_problem(ctx, p);
+        // the target index (host BVH build) and the problem plan are
+        // independent host work: overlap them
+        std::exception_ptr bvh_err;
+        std::thread bvh([&] {
+            try {
+                ctx->bvh.build(p->target, p->m);
+            } catch (...) {
+                bvh_err = std::current_exception();
+            }
+        });
+        std::exception_ptr plan_err;
+        try {
+            set_problem(ctx, p);
+        } catch (...) {
+            plan_err = std::current_exception();
+        }
+        bvh.join();
+        if (bvh_err) std::rethrow_exception(bvh_err);
+        if (plan_err) std::rethrow_exception(plan_err);
+        set_target(ctx, p->target, p->m, true);
         run_register(ctx, *cfg, out_X, out_deformed);
     });
 }
