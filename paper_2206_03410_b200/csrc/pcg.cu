@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     const int nel = nrows * 12;
     const int my_rc = threadIdx.x % 12, my_r = my_rc / 3, my_c = my_rc % 3;
     double xr[EPT], br[EPT], rr[EPT], zr[EPT], pr[EPT];
-    int el_row[EPT];
+    int el_row[EPT], el_b0[EPT], el_b1[EPT];  // row, block range in the CTA's K
     size_t el_g[EPT];
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
@@ -592,6 +592,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         const bool live = e < nel;
         const int lr = live ? e / 12 : 0;
         el_row[k] = live ? lr : -1;
+        el_b0[k] = a.row_ptr[r0 + lr] - kb0;
+        el_b1[k] = live ? a.row_ptr[r0 + lr + 1] - kb0 : el_b0[k];
         el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + my_rc;
         xr[k] = live ? a.X[el_g[k]] : 0.0;
         br[k] = live ? a.B[el_g[k]] : 0.0;
@@ -623,27 +625,27 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         __syncthreads();
     };
     auto spmv = [&](int k) -> double {
-        const int lr = el_row[k];
-        if (lr < 0) return 0.0;
-        const int j = r0 + lr;
-        const int b0 = a.row_ptr[j] - kb0, b1 = a.row_ptr[j + 1] - kb0;
+        const int b0 = el_b0[k], b1 = el_b1[k];  // empty range for dead elements
         // two independent chains (even / odd blocks) halve the FMA latency chain
         double acc0 = 0.0, acc1 = 0.0;
         int b = b0;
         for (; b + 1 < b1; b += 2) {
             const int c0 = sh.col[b], c1 = sh.col[b + 1];
             const double* k0 = sh.K + static_cast<size_t>(b) * 16 + my_r * 4;
-            const double* k1 = k0 + 16;
+            const double2 ka0 = *reinterpret_cast<const double2*>(k0);
+            const double2 ka1 = *reinterpret_cast<const double2*>(k0 + 2);
+            const double2 kb0 = *reinterpret_cast<const double2*>(k0 + 16);
+            const double2 kb1 = *reinterpret_cast<const double2*>(k0 + 18);
             const double* v0 = sh.ext + c0 * 12 + my_c;
             const double* v1 = sh.ext + c1 * 12 + my_c;
-            acc0 = fma(k0[0], v0[0], acc0);
-            acc1 = fma(k1[0], v1[0], acc1);
-            acc0 = fma(k0[1], v0[3], acc0);
-            acc1 = fma(k1[1], v1[3], acc1);
-            acc0 = fma(k0[2], v0[6], acc0);
-            acc1 = fma(k1[2], v1[6], acc1);
-            acc0 = fma(k0[3], v0[9], acc0);
-            acc1 = fma(k1[3], v1[9], acc1);
+            acc0 = fma(ka0.x, v0[0], acc0);
+            acc1 = fma(kb0.x, v1[0], acc1);
+            acc0 = fma(ka0.y, v0[3], acc0);
+            acc1 = fma(kb0.y, v1[3], acc1);
+            acc0 = fma(ka1.x, v0[6], acc0);
+            acc1 = fma(kb1.x, v1[6], acc1);
+            acc0 = fma(ka1.y, v0[9], acc0);
+            acc1 = fma(kb1.y, v1[9], acc1);
         }
         if (b < b1) {
             const double* kk = sh.K + static_cast<size_t>(b) * 16 + my_r * 4;
