@@ -55,207 +55,433 @@ __device__ __forceinline__ void node_offset(const PcgArgs& a, int node, double d
     for (int k = 0; k < 3; ++k) d[k] = a.node_pos[3 * node + k] - a.agg_center[3 * g + k];
 }
 
+// Branch-free FP64 reciprocal / quotient: hardware approximation + two Newton
+// steps (full precision for normal operands; deterministic, not IEEE-rounded).
+// The PCG scalars need no correctly rounded division, and the library
+// routine's special-case branch serialises the three columns.
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double div_nr(double n, double d) {
+    const double r = rcp_nr(d);
+    const double q = n * r;
+    return fma(r, fma(-d, q, n), q);
+}
+
 // ---------------------------------------------------------------- blocked Gauss-Jordan
 // In-place inverse of nm SPD matrices held in shared memory (matrix k: n_k x
 // n_k with n_k = 4 * blocks_k, leading dimension ld, base A + k * msz), all
 // processed together by the whole CTA, 4 pivots (one node block) at a time:
-//   P = A_TT^{-1} (4x4, one thread per matrix; a pivot <= drop * dmax_k drops
-//       that mode: zero row and column),
+//   P = A_TT^{-1} (4x4, one thread per matrix, reciprocal + Newton; a pivot
+//       <= drop * dmax_k drops that mode: zero row and column),
 //   R = P A_T:,  C = A_:T,
 //   A_ij -= C_i R_j,  A_iT = -C_i P,  A_Tj = R_j,  A_TT = P.
-// Three barriers per block step; every element update is a rank-4 FMA chain.
-// Fixed operation order: deterministic. Scratch: pb[nm*16], cb[nm*4*ld] (C
-// rows), rb[nm*4*ld] (R), blocks[nm] (4x4 blocks per matrix), dmax[nm].
+// Three barriers per block step; the element updates are spread over every
+// thread of the CTA (row-major flattening over the matrices' rows x ncmax
+// columns). Fixed operation order: deterministic. Scratch: pb[nm*16],
+// cb[nm*4*ld] (C, s-major), rb[nm*4*ld] (R), blocks[nm], dmax[nm].
 __device__ void block_gj_inverse(double* A, int nm, const int* blocks, int ld, size_t msz, double* pb, double* cb,
-                                 double* rb, const double* dmax, double drop) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+                                 double* rb, const double* dmax, double drop, long long* prof = nullptr) {
+    long long tq = clock64();
+    auto gprobe = [&](int slot) {
+        if (prof != nullptr && threadIdx.x == 0) {
+            const long long t = clock64();
+            prof[slot] += t - tq;
+            tq = t;
+        }
+    };
     int nb_max = 0, rows_total = 0;
     for (int k = 0; k < nm; ++k) {
         nb_max = max(nb_max, blocks[k]);
         rows_total += 4 * blocks[k];
     }
+    // element (gi, j) of the flattened matrix rows -> matrix k, local row i
+    auto locate = [&](int gi, int& k, int& i) {
+        int base = 0;
+        k = 0;
+        while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
+        i = gi - base;
+    };
     for (int T = 0; T < nb_max; ++T) {
         const int t0 = 4 * T;
-        // phase 1: P per matrix (thread k), raw C and row block T into cb / rb
+        // phase 1: P per matrix (thread k); raw C and row block T into cb / rb
         if (threadIdx.x < nm && T < blocks[threadIdx.x]) {
             const int k = threadIdx.x;
             const double* Ak = A + k * msz;
             double m[4][4], inv[4][4];
+#pragma unroll
             for (int r = 0; r < 4; ++r)
+#pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     m[r][c] = Ak[(t0 + r) * ld + t0 + c];
                     inv[r][c] = r == c ? 1.0 : 0.0;
                 }
             bool live[4];
+#pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const double piv = m[q][q];
                 live[q] = piv > drop * dmax[k];
-                const double d = live[q] ? 1.0 / piv : 0.0;
+                const double d = live[q] ? rcp_nr(piv) : 0.0;
+#pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     m[q][c] *= d;
                     inv[q][c] *= d;
                 }
+#pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     if (r == q) continue;
                     const double f = m[r][q];
+#pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         m[r][c] -= f * m[q][c];
                         inv[r][c] -= f * inv[q][c];
                     }
                 }
             }
+#pragma unroll
             for (int r = 0; r < 4; ++r)
+#pragma unroll
                 for (int c = 0; c < 4; ++c) pb[k * 16 + r * 4 + c] = (live[r] && live[c]) ? inv[r][c] : 0.0;
         }
         for (int gi = threadIdx.x; gi < rows_total; gi += blockDim.x) {
-            int k = 0, base = 0;
-            while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
+            int k, i;
+            locate(gi, k, i);
             if (T >= blocks[k]) continue;
-            const int i = gi - base;
             const double* Ai = A + k * msz + static_cast<size_t>(i) * ld;
+#pragma unroll
             for (int s = 0; s < 4; ++s) {
-                cb[k * 4 * ld + s * ld + i] = Ai[t0 + s];                           // C[i][s], stored s-major
+                cb[k * 4 * ld + s * ld + i] = Ai[t0 + s];                                         // C[i][s]
                 rb[k * 4 * ld + s * ld + i] = A[k * msz + static_cast<size_t>(t0 + s) * ld + i];  // row T+s, column i
             }
         }
+        gprobe(24);
         __syncthreads();
+        gprobe(25);
         // phase 2: R = P * (row block), in place in rb
         for (int gi = threadIdx.x; gi < rows_total; gi += blockDim.x) {
-            int k = 0, base = 0;
-            while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
+            int k, j;
+            locate(gi, k, j);
             if (T >= blocks[k]) continue;
-            const int j = gi - base;
             double* rk = rb + k * 4 * ld;
             const double* P = pb + k * 16;
             const double x0 = rk[j], x1 = rk[ld + j], x2 = rk[2 * ld + j], x3 = rk[3 * ld + j];
+#pragma unroll
             for (int r = 0; r < 4; ++r) rk[r * ld + j] = P[r * 4] * x0 + P[r * 4 + 1] * x1 + P[r * 4 + 2] * x2 + P[r * 4 + 3] * x3;
         }
         __syncthreads();
-        // phase 3: rank-4 update, one warp per row, lanes over columns
-        for (int gi = w; gi < rows_total; gi += nw) {
-            int k = 0, base = 0;
-            while (gi >= base + 4 * blocks[k]) base += 4 * blocks[k++];
-            if (T >= blocks[k]) continue;
-            const int i = gi - base, nk = 4 * blocks[k];
-            double* Ai = A + k * msz + static_cast<size_t>(i) * ld;
-            const double* ck = cb + k * 4 * ld;
-            const double* rk = rb + k * 4 * ld;
-            const double* P = pb + k * 16;
-            const bool in_t = i >= t0 && i < t0 + 4;
-            const double c0 = ck[i], c1 = ck[ld + i], c2 = ck[2 * ld + i], c3 = ck[3 * ld + i];
-            for (int j = lane; j < nk; j += 32) {
-                const bool jt = j >= t0 && j < t0 + 4;
-                double v;
-                if (in_t && jt) v = P[(i - t0) * 4 + (j - t0)];
-                else if (in_t) v = rk[(i - t0) * ld + j];
-                else if (jt) {
-                    const int q = j - t0;
-                    v = -(c0 * P[q] + c1 * P[4 + q] + c2 * P[8 + q] + c3 * P[12 + q]);
-                } else {
-                    v = Ai[j] - (c0 * rk[j] + c1 * rk[ld + j] + c2 * rk[2 * ld + j] + c3 * rk[3 * ld + j]);
+        gprobe(26);
+        // phase 3: rank-4 update, one warp per row (matrix and row located
+        // once), lanes over columns
+        {
+            const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+            for (int gi = w; gi < rows_total; gi += nw) {
+                int k, i;
+                locate(gi, k, i);
+                if (T >= blocks[k]) continue;
+                const int nk = 4 * blocks[k];
+                double* Ai = A + k * msz + static_cast<size_t>(i) * ld;
+                const double* ck = cb + k * 4 * ld;
+                const double* rk = rb + k * 4 * ld;
+                const double* P = pb + k * 16;
+                const bool in_t = i >= t0 && i < t0 + 4;
+                const double c0 = ck[i], c1 = ck[ld + i], c2 = ck[2 * ld + i], c3 = ck[3 * ld + i];
+                for (int j = lane; j < nk; j += 32) {
+                    const bool jt = j >= t0 && j < t0 + 4;
+                    double v;
+                    if (in_t && jt) {
+                        v = P[(i - t0) * 4 + (j - t0)];
+                    } else if (in_t) {
+                        v = rk[(i - t0) * ld + j];
+                    } else if (jt) {
+                        const int q = j - t0;
+                        v = -(c0 * P[q] + c1 * P[4 + q] + c2 * P[8 + q] + c3 * P[12 + q]);
+                    } else {
+                        v = Ai[j] - (c0 * rk[j] + c1 * rk[ld + j] + c2 * rk[2 * ld + j] + c3 * rk[3 * ld + j]);
+                    }
+                    Ai[j] = v;
                 }
-                Ai[j] = v;
             }
         }
+        gprobe(27);
         __syncthreads();
+        gprobe(28);
     }
 }
 
 // ---------------------------------------------------------------- coarse setup
-// CTA c: partial[c][k][h*4+l] = sum over its rows a and blocks (a,b) with b in
-// aggregate h of psi_k(a)^T K_ab psi_l(b). The CTA's blocks are first staged
-// in shared memory with their row/column offsets and column aggregate; then one
-// thread per output entry scans them in BSR order: deterministic, no atomics.
+// CTA c: for each aggregate h its rows' columns touch (touch list t < nt),
+// partial[c][t][k*4+l] = sum over the CTA's blocks (a,b) with b in h of
+// psi_k(a)^T K_ab psi_l(b). One thread per block forms its 4x4 projection
+// (staged in shared memory), then 8 lanes per output sum the blocks of that
+// aggregate (lane-strided, butterfly-combined): deterministic, no atomics.
 __global__ void __launch_bounds__(kCoarseThreads) coarse_partial_kernel(PcgArgs a, double* __restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int c = blockIdx.x;
     const int r0 = a.row_begin[c], r1 = a.row_begin[c + 1];
     const int kb0 = a.row_ptr[r0], nkb = a.row_ptr[r1] - kb0;
-    const int nc = 4 * a.n_agg;
-    double* Kb = reinterpret_cast<double*>(smem_raw);         // nkb*16
-    double* da = Kb + 16 * static_cast<size_t>(nkb);          // nkb*3 row-node offsets
-    double* db = da + 3 * static_cast<size_t>(nkb);           // nkb*3 col-node offsets
-    int* hb = reinterpret_cast<int*>(db + 3 * static_cast<size_t>(nkb));  // nkb col aggregate
-    for (int i = threadIdx.x; i < nkb * 16; i += blockDim.x) Kb[i] = a.K[static_cast<size_t>(kb0) * 16 + i];
-    for (int j = r0 + (threadIdx.x >> 5); j < r1; j += blockDim.x >> 5) {
-        const int na = a.row_node[j];
-        double d[3];
+    const int t0 = a.touch_off[c], nt = a.touch_off[c + 1] - t0;
+    double* Pb = reinterpret_cast<double*>(smem_raw);                 // nkb*16
+    int* tb = reinterpret_cast<int*>(Pb + 16 * static_cast<size_t>(nkb));  // nkb: touched index of the column aggregate
+    int* rowof = tb + nkb;                                            // nkb: local row of the block
+    __shared__ int s_touch[64];
+    for (int t = threadIdx.x; t < nt && t < 64; t += blockDim.x) s_touch[t] = a.touch_agg[t0 + t];
+    for (int j = r0 + threadIdx.x; j < r1; j += blockDim.x)
+        for (int b = a.row_ptr[j]; b < a.row_ptr[j + 1]; ++b) rowof[b - kb0] = j;
+    __syncthreads();
+    for (int lb = threadIdx.x; lb < nkb; lb += blockDim.x) {
+        const int na = a.row_node[rowof[lb]], nb = a.col[kb0 + lb];
+        double d[3], e[3];
         node_offset(a, na, d);
-        for (int b = a.row_ptr[j] + (threadIdx.x & 31); b < a.row_ptr[j + 1]; b += 32) {
-            const int nb = a.col[b];
-            double e[3];
-            node_offset(a, nb, e);
-            const int lb = b - kb0;
-            for (int t = 0; t < 3; ++t) {
-                da[3 * lb + t] = d[t];
-                db[3 * lb + t] = e[t];
-            }
-            hb[lb] = a.node_agg[nb];
+        node_offset(a, nb, e);
+        const int hb = a.node_agg[nb];
+        int t = 0;
+        while (t < nt - 1 && s_touch[t] != hb) ++t;
+        tb[lb] = t;
+        const double* K = a.K + static_cast<size_t>(kb0 + lb) * 16;
+        double k4[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) k4[q] = K[q];
+        double u[4][4];  // u = K_ab psi(b)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+            for (int l = 0; l < 3; ++l) u[r][l] = k4[r * 4 + l] + e[l] * k4[r * 4 + 3];
+            u[r][3] = k4[r * 4 + 3];
+        }
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) Pb[lb * 16 + k * 4 + l] = u[k][l] + d[k] * u[3][l];
+            Pb[lb * 16 + 12 + l] = u[3][l];
         }
     }
     __syncthreads();
-    for (int o = threadIdx.x; o < 4 * nc; o += blockDim.x) {
-        const int k = o / nc, hl = o - k * nc, h = hl >> 2, l = hl & 3;
-        double acc = 0.0;
-        for (int lb = 0; lb < nkb; ++lb) {
-            if (hb[lb] != h) continue;
-            const double* K = Kb + 16 * lb;
-            double u[4];  // u = K_ab psi_l(b)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) u[r] = l < 3 ? K[r * 4 + l] + db[3 * lb + l] * K[r * 4 + 3] : K[r * 4 + 3];
-            acc += k < 3 ? u[k] + da[3 * lb + k] * u[3] : u[3];
+    const int l8 = threadIdx.x & 7;
+    for (int o0 = 0; o0 < nt * 16; o0 += blockDim.x >> 3) {  // uniform trip count: full-warp shuffles
+        const int o = o0 + (threadIdx.x >> 3);
+        double s = 0.0;
+        if (o < nt * 16) {
+            const int t = o >> 4, kl = o & 15;
+            for (int lb = l8; lb < nkb; lb += 8)
+                if (tb[lb] == t) s += Pb[lb * 16 + kl];
         }
-        partial[(static_cast<size_t>(c) * 4 + k) * nc + hl] = acc;
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (l8 == 0 && o < nt * 16) partial[(static_cast<size_t>(c) * a.max_touch + (o >> 4)) * 16 + (o & 15)] = s;
     }
 }
 
-// One CTA: K0 = sum of the partials of each aggregate's CTAs (fixed order),
-// symmetrised, inverted in place by Gauss-Jordan (SPD: no pivoting needed);
-// modes with a vanishing pivot are dropped (zero rows / columns). Warp w owns
-// rows w, w+nw, ...; lanes own columns: no index division in the inner loop.
-__global__ void __launch_bounds__(kCoarseThreads) coarse_invert_kernel(PcgArgs a, const double* __restrict__ partial,
-                                                                   double* __restrict__ inv, int grid) {
+// One CTA: K0 (g*4+k, h*4+l) = sum over aggregate g's CTAs (in order) of
+// their partial for touched aggregate h; symmetrised and inverted in place by
+// block Gauss-Jordan on 4x4 node blocks (SPD; modes with a vanishing pivot are
+// dropped). Each thread keeps up to kCiTiles 4x4 tiles of K0 in registers for
+// the whole inversion; per pivot step only the pivot row / column blocks go
+// through shared memory (double-buffered, two barriers per step; stored
+// entry-major, X[q * nb + j], so lanes with consecutive tiles hit distinct
+// banks: a 16-double stride put every lane of a warp on one bank), so the
+// step costs one 4x4x4 product per tile instead of a shared-memory pass over
+// the matrix. Deterministic.
+constexpr int kCiThreads = 512;
+constexpr int kCiTiles = 2;  // n_agg^2 <= kCiThreads * kCiTiles  (n_agg <= 32)
+__device__ __forceinline__ void mm4(const double* a, const double* b, double* c) {  // c = a b (row-major 4x4)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            c[r * 4 + q] = a[r * 4] * b[q] + a[r * 4 + 1] * b[4 + q] + a[r * 4 + 2] * b[8 + q] + a[r * 4 + 3] * b[12 + q];
+}
+__global__ void __launch_bounds__(kCiThreads) coarse_invert_kernel(PcgArgs a, const double* __restrict__ partial,
+                                                               double* __restrict__ inv, int grid) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int nc = 4 * a.n_agg;
-    double* A = reinterpret_cast<double*>(smem_raw);  // nc*nc
-    double* colk = A + nc * nc;                       // 4 * nc
-    double* rowk = colk + 4 * nc;                     // 4 * nc
-    __shared__ double s_dmax, s_pb[16];
-    __shared__ int s_blocks;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int i = w; i < nc; i += nw) {
-        const int g = i >> 2, k = i & 3;
-        for (int j = lane; j < nc; j += 32) {
-            double sum = 0.0;
-            const int c0 = g * a.agg_ctas, c1 = min((g + 1) * a.agg_ctas, grid);
-            for (int cb = c0; cb < c1; cb += 8) {  // 8 loads in flight, summed in CTA order
-                double x[8];
+    const int nb = a.n_agg, nc = 4 * nb, mt = a.max_touch;
+    double* S = reinterpret_cast<double*>(smem_raw);             // nc*nc (symmetrisation)
+    double* rowb = S + static_cast<size_t>(nc) * nc;              // 2 x nb x 16: pivot row blocks A_Tj
+    double* colb = rowb + 2 * 16 * nb;                            // 2 x nb x 16: pivot column blocks A_iT
+    double* Rb = colb + 2 * 16 * nb;                              // 2 x nb x 16: R_j = P A_Tj
+    double* Pb = Rb + 2 * 16 * nb;                                // 2 x 16
+    int* touch = reinterpret_cast<int*>(Pb + 32);                 // grid * mt
+    __shared__ double s_dmax[kCiThreads / 32];
+    long long tq = clock64();
+    auto cprobe = [&](int slot) {
+        if (a.prof != nullptr && threadIdx.x == 0) {
+            const long long t = clock64();
+            a.prof[slot] += t - tq;
+            tq = t;
+        }
+    };
+    for (int i = threadIdx.x; i < grid * mt; i += blockDim.x) {
+        const int c = i / mt, t = i - c * mt;
+        const int t0 = a.touch_off[c], nt = a.touch_off[c + 1] - t0;
+        touch[i] = t < nt ? a.touch_agg[t0 + t] : -1;
+    }
+    __syncthreads();
+    double A[kCiTiles][16];
+    int bi[kCiTiles], bj[kCiTiles];
+    // fill: tile (g, h) = sum over g's CTAs (CTA order) of their partial for h
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    x[u] = cb + u < c1 ? __ldcg(partial + (static_cast<size_t>(cb + u) * 4 + k) * nc + j) : 0.0;
+    for (int u = 0; u < kCiTiles; ++u) {
+        const int tile = threadIdx.x + u * blockDim.x;
+        bi[u] = tile < nb * nb ? tile / nb : -1;
+        bj[u] = tile < nb * nb ? tile - bi[u] * nb : -1;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) sum += x[u];
+        for (int q = 0; q < 16; ++q) A[u][q] = 0.0;
+        if (bi[u] < 0) continue;
+        const int c0 = bi[u] * a.agg_ctas, c1 = min(c0 + a.agg_ctas, grid);
+        for (int c = c0; c < c1; ++c) {
+            int t = 0;
+            while (t < mt && touch[c * mt + t] != bj[u]) ++t;
+            if (t == mt) continue;
+            const double2* src = reinterpret_cast<const double2*>(partial + (static_cast<size_t>(c) * mt + t) * 16);
+            double2 x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x[q] = __ldcg(src + q);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                A[u][2 * q] += x[q].x;
+                A[u][2 * q + 1] += x[q].y;
             }
-            A[i * nc + j] = sum;
         }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) S[(bi[u] * 4 + r) * nc + bj[u] * 4 + q] = A[u][r * 4 + q];
     }
     __syncthreads();
-    for (int i = w; i < nc; i += nw)
-        for (int j = lane; j < i; j += 32) {
-            const double v = 0.5 * (A[i * nc + j] + A[j * nc + i]);
-            A[i * nc + j] = v;
-            A[j * nc + i] = v;
-        }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double m = 0.0;
-        for (int i = 0; i < nc; ++i) m = fmax(m, fabs(A[i * nc + i]));
-        s_dmax = m;
-        s_blocks = nc / 4;
+    cprobe(20);
+    double dm = 0.0;
+#pragma unroll
+    for (int u = 0; u < kCiTiles; ++u) {
+        if (bi[u] < 0) continue;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = bi[u] * 4 + r, j = bj[u] * 4 + q;
+                A[u][r * 4 + q] = 0.5 * (S[i * nc + j] + S[j * nc + i]);
+                if (i == j) dm = fmax(dm, fabs(A[u][r * 4 + q]));
+            }
     }
+    dm = warp_max(dm);
+    if ((threadIdx.x & 31) == 0) s_dmax[threadIdx.x >> 5] = dm;
     __syncthreads();
-    block_gj_inverse(A, 1, &s_blocks, nc, 0, s_pb, colk, rowk, &s_dmax, 1e-12);
-    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) inv[o] = A[o];
+    double dmax = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) dmax = fmax(dmax, s_dmax[w]);
+    const double drop = 1e-12 * dmax;
+    cprobe(21);
+    for (int T = 0; T < nb; ++T) {
+        const int par = T & 1;
+        double* rowT = rowb + par * 16 * nb;
+        double* colT = colb + par * 16 * nb;
+        double* RT = Rb + par * 16 * nb;
+        double* PT = Pb + par * 16;
+        // phase A: pivot inverse (4x4 Gauss-Jordan, dropped modes zeroed) and
+        // the pivot row / column blocks
+#pragma unroll
+        for (int u = 0; u < kCiTiles; ++u) {
+            if (bi[u] == T && bj[u] == T) {
+                double m[4][4], iv[4][4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        m[r][c] = A[u][r * 4 + c];
+                        iv[r][c] = r == c ? 1.0 : 0.0;
+                    }
+                bool live[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    live[q] = m[q][q] > drop;
+                    const double d = live[q] ? rcp_nr(m[q][q]) : 0.0;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        m[q][c] *= d;
+                        iv[q][c] *= d;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (r == q) continue;
+                        const double f = m[r][q];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            m[r][c] -= f * m[q][c];
+                            iv[r][c] -= f * iv[q][c];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) PT[r * 4 + c] = (live[r] && live[c]) ? iv[r][c] : 0.0;
+            }
+            if (bi[u] == T)
+#pragma unroll
+                for (int q = 0; q < 16; ++q) rowT[q * nb + bj[u]] = A[u][q];
+            if (bj[u] == T)
+#pragma unroll
+                for (int q = 0; q < 16; ++q) colT[q * nb + bi[u]] = A[u][q];
+        }
+        cprobe(24);
+        __syncthreads();
+        cprobe(25);
+        // phase B: R_j = P A_Tj
+        for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+            double p[16], r[16], o[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                p[q] = PT[q];
+                r[q] = rowT[q * nb + j];
+            }
+            mm4(p, r, o);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) RT[q * nb + j] = o[q];
+        }
+        cprobe(26);
+        __syncthreads();
+        cprobe(27);
+        // phase C: A_ij -= C_i R_j; A_Tj = R_j; A_iT = -C_i P; A_TT = P
+#pragma unroll
+        for (int u = 0; u < kCiTiles; ++u) {
+            if (bi[u] < 0) continue;
+            if (bi[u] == T) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) A[u][q] = bj[u] == T ? PT[q] : RT[q * nb + bj[u]];
+                continue;
+            }
+            double cm[16], o[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) cm[q] = colT[q * nb + bi[u]];
+            if (bj[u] == T) {
+                double p[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) p[q] = PT[q];
+                mm4(cm, p, o);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) A[u][q] = -o[q];
+            } else {
+                double r[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) r[q] = RT[q * nb + bj[u]];
+                mm4(cm, r, o);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) A[u][q] -= o[q];
+            }
+        }
+        cprobe(28);
+    }
+    cprobe(22);
+#pragma unroll
+    for (int u = 0; u < kCiTiles; ++u) {
+        if (bi[u] < 0) continue;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) inv[static_cast<size_t>(bi[u] * 4 + r) * nc + bj[u] * 4 + q] = A[u][r * 4 + q];
+    }
 }
 
 // ---------------------------------------------------------------- subdomain inverses
@@ -317,18 +543,17 @@ struct Shared {
     double* K;       // nkb*16
     int* col;        // nkb
     double* Minv;    // per subdomain chunk: dense inverse of its 4s x 4s diagonal block (leading dim sub_ld)
-    double* zz;      // nrows*12: M_sub r
+    double* zz;      // nrows*12: M_sub v
     int* cstart;     // chunk row ranges [cstart[k], cstart[k+1])
     int* rchunk;     // own row -> chunk
-    double* rex;     // nrows*12 exchange of r
-    double* off;     // nrows*3 node offsets to the aggregate centre
-    double* cinv;    // 4 x nc rows of K0^-1 for the own aggregate
-    double* rho;     // nc x 3 coarse residual (replicated)
-    double* ptq;     // nc x 3 aggregate sums of Psi^T w (this iteration)
-    double* sig;     // nc x 3 Psi^T s (replicated recurrence)
-    double* red;     // 16 warps x kQ
+    double* rex;     // nrows*12: M_sub input
+    double* offx;    // operand rows x 3: node offset to its aggregate centre
+    int* tl;         // operand rows: index of its aggregate in the CTA's touched list
+    double* cinv;    // touched aggregates x 4 rows of K0^-1 (nc each)
+    double* yt;      // touched aggregates x 12: coarse correction
+    double* ptq;     // nc x 3 aggregate sums of Psi^T v (replicated)
+    double* red;     // kRedDoubles: reduction scratch
     double* bcast;   // kQ
-    double* y;       // 12: own aggregate coarse correction
     double* ext;     // (own rows + halo) x 12: the SpMV operand staged from L2
 };
 
@@ -450,9 +675,128 @@ __device__ __forceinline__ void aggregate_sums(const PcgArgs& a, const double* _
     }
 }
 
+// Per-iteration CTA partials of the 7 per-thread values (gamma, delta, max|r|
+// and the 4 Psi^T w mode sums; all of a thread's elements share one column c =
+// threadIdx % 3). Each value goes to shared memory grouped by column class,
+// then one half-warp per output slot sums its 128 (or, for max|r|, 384)
+// entries in a fixed order: 7 shared stores per thread instead of a 32-slot
+// shuffle transpose. Slots: 0-2 gamma by column, 3-5 delta, 6 max|r|,
+// 7 + 3m + c mode m (as grid_totals / aggregate_sums read them).
+constexpr int kClass = kPcgThreads / 3;
+// The iteration partials are written kPartReplicas times and each CTA reads
+// replica (cta % kPartReplicas): right after the barrier all CTAs read the
+// same few KB, and replication spreads those reads over more L2 slices.
+constexpr int kPartReplicas = 8;
+constexpr int kRedDoubles = 7 * kPcgThreads;
+static_assert(kRedDoubles >= 32 * kQ, "reduction scratch");
+__device__ __forceinline__ void iter_partials(double g, double dl, double rmx, const double ps[4], int nq, double* red,
+                                              double* part) {
+    const int t = threadIdx.x, c = t % 3, i = t / 3;
+    red[(0 * 3 + c) * kClass + i] = g;
+    red[(1 * 3 + c) * kClass + i] = dl;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) red[((2 + m) * 3 + c) * kClass + i] = ps[m];
+    red[18 * kClass + t] = rmx;
+    __syncthreads();
+    const int s = t >> 4, hl = t & 15;
+    const bool mx = s == 6;
+    double v = 0.0;
+    if (s < nq) {
+        if (mx) {
+            double x[kPcgThreads / 16];
+#pragma unroll
+            for (int k = 0; k < kPcgThreads / 16; ++k) x[k] = red[18 * kClass + hl + 16 * k];
+            v = x[0];
+#pragma unroll
+            for (int k = 1; k < kPcgThreads / 16; ++k) v = fmax(v, x[k]);
+        } else {
+            const int blk = s < 6 ? s : s - 1;
+            double x[kClass / 16];
+#pragma unroll
+            for (int k = 0; k < kClass / 16; ++k) x[k] = red[blk * kClass + hl + 16 * k];
+            v = x[0];
+#pragma unroll
+            for (int k = 1; k < kClass / 16; ++k) v += x[k];
+        }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v = op2(mx, v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (hl == 0 && s < nq) {
+        const size_t rs = static_cast<size_t>(kQ) * ((gridDim.x + 7) & ~7);
+#pragma unroll
+        for (int r = 0; r < kPartReplicas; ++r) part[r * rs + s * ((gridDim.x + 7) & ~7) + blockIdx.x] = v;
+    }
+}
+
+// Grid totals of slots 0-6 (warps 0-6, one slot each) and the aggregate sums
+// of the Psi^T slots (one output per thread) with every L2 load issued before
+// any is combined: one round trip. The partials are slot-major (part[s][cta],
+// row length round_up(G, 8)): every CTA reads the same few KB right after the
+// barrier, so the number of L2 sector requests, not latency, sets the cost;
+// this layout makes a slot's grid total 37 sectors and an aggregate sum two
+// 32-byte vector loads; the partials are also replicated (kPartReplicas). Same summation order as grid_totals / aggregate_sums.
+__device__ __forceinline__ void iter_totals(const PcgArgs& a, const double* __restrict__ part, int G, double* bcast,
+                                            double* ptq) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nc = 4 * a.n_agg, Gp = (G + 7) & ~7;
+    part += static_cast<size_t>(blockIdx.x % kPartReplicas) * kQ * Gp;  // this CTA's replica
+    const bool tot = w < 7;
+    double xt[kMaxGridLoads];
+#pragma unroll
+    for (int i = 0; i < kMaxGridLoads; ++i) {
+        const int g = lane + 32 * i;
+        xt[i] = tot && g < G ? __ldcg(part + w * Gp + g) : 0.0;
+    }
+    double2 xa[4];
+    const bool fast = a.use_coarse && a.agg_ctas == 8;
+    for (int o = threadIdx.x; a.use_coarse && o < nc * 3; o += blockDim.x) {
+        const int g = o / 12, kc = o % 12;
+        const int c0 = g * a.agg_ctas, c1 = min(c0 + a.agg_ctas, G);
+        const double* src = part + (7 + kc) * Gp + c0;
+        if (fast && o == static_cast<int>(threadIdx.x)) {  // 8 CTAs, 64-byte aligned, zero padded
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xa[i] = __ldcg(reinterpret_cast<const double2*>(src) + i);
+            continue;
+        }
+        double s = 0.0;
+        for (int cb = c0; cb < c1; cb += 8) {
+            double x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = cb + i < c1 ? __ldcg(part + (7 + kc) * Gp + cb + i) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s += x[i];
+        }
+        ptq[o] = s;
+    }
+    if (tot) {
+        const bool mx = w == 6;
+        double v = xt[0];
+#pragma unroll
+        for (int i = 1; i < kMaxGridLoads; ++i) v = mx ? fmax(v, xt[i]) : v + xt[i];
+        v = mx ? warp_max(v) : warp_sum(v);
+        if (lane == 0) bcast[w] = v;
+    }
+    if (fast && static_cast<int>(threadIdx.x) < nc * 3) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            s += xa[i].x;
+            s += xa[i].y;
+        }
+        ptq[threadIdx.x] = s;
+    }
+}
+
 template <int EPT>
-__global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
+__global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     cg::grid_group grid = cg::this_grid();
+    // The arguments are read from shared memory inside the loop: every grid
+    // barrier's gpu-scope fence invalidates the SM's caches, and a constant
+    // bank reload after it cost ~1.5K cycles per iteration (NRR_PROF probes).
+    __shared__ PcgArgs s_args;
+    if (threadIdx.x == 0) s_args = a_param;
+    __syncthreads();
+    const PcgArgs& a = s_args;
     const long long t_entry = clock64();
     long long t_probe = t_entry;
     const bool sprof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
@@ -469,38 +813,37 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     const int nrows = r1 - r0;
     const int kb0 = a.row_ptr[r0], nkb = a.row_ptr[r1] - kb0;
     const int nc = 4 * a.n_agg;
-    const int my_agg = cta / a.agg_ctas;
+    const int e0 = a.ext_off[cta], n_ext = a.ext_off[cta + 1] - e0;
+    const int t0 = a.touch_off[cta], nt = a.touch_off[cta + 1] - t0;
     Shared sh;
     {
         double* p = reinterpret_cast<double*>(smem_raw);
         sh.red = p;
-        p += 32 * kQ;
+        p += kRedDoubles;
         sh.bcast = p;
         p += kQ;
-        sh.y = p;
-        p += 16;
-        sh.Minv = p;  // offset 32*kQ + kQ + 16 doubles: even -> 16-byte aligned
+        sh.Minv = p;  // offset kRedDoubles + kQ doubles: even -> 16-byte aligned
         p += static_cast<size_t>(a.sub_chunks) * 4 * a.sub_rows * a.sub_ld;
         sh.zz = p;
         p += 12 * a.max_rows;
+        sh.rex = p;
+        p += 12 * a.max_rows;
+        sh.offx = p;
+        p += 3 * static_cast<size_t>(a.max_ext);
+        sh.cinv = p;
+        p += 4 * static_cast<size_t>(a.max_touch) * nc;
+        sh.yt = p;
+        p += 12 * a.max_touch;
+        sh.ptq = p;
+        p += 3 * kCoarseMax;
+        sh.ext = p;
+        p += 12 * static_cast<size_t>(a.max_ext);
         sh.cstart = reinterpret_cast<int*>(p);
         p += (a.sub_chunks + 2) / 2;
         sh.rchunk = reinterpret_cast<int*>(p);
         p += (a.max_rows + 1) / 2;
-        sh.rex = p;
-        p += 12 * a.max_rows;
-        sh.off = p;
-        p += (3 * a.max_rows + 1) & ~1;  // keep the K region 16-byte aligned
-        sh.cinv = p;
-        p += 4 * kCoarseMax;
-        sh.rho = p;
-        p += 3 * kCoarseMax;
-        sh.ptq = p;
-        p += 3 * kCoarseMax;
-        sh.sig = p;
-        p += 3 * kCoarseMax;
-        sh.ext = p;
-        p += 12 * static_cast<size_t>(a.max_ext);
+        sh.tl = reinterpret_cast<int*>(p);
+        p += (a.max_ext + 1) / 2;
         if ((p - reinterpret_cast<double*>(smem_raw)) & 1) ++p;  // 16-byte aligned K
         if (a.k_in_smem) {
             sh.K = p;
@@ -518,19 +861,24 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         for (int i = threadIdx.x; i < nkb; i += blockDim.x) sh.col[i] = a.colx[kb0 + i];
     }
     probe(10);  // K -> smem issued
+    // coarse rows of the aggregates this CTA's operand rows touch, and every
+    // operand row's offset to its aggregate centre (own rows come first)
     if (a.use_coarse) {
-        for (int i = threadIdx.x; i < 4 * nc; i += blockDim.x) {
-            const int k = i / nc, j = i % nc;
-            sh.cinv[i] = a.coarse_inv[static_cast<size_t>(my_agg * 4 + k) * nc + j];
+        for (int i = threadIdx.x; i < nt * 4 * nc; i += blockDim.x) {
+            const int t = i / (4 * nc), kj = i - t * 4 * nc;
+            sh.cinv[i] = a.coarse_inv[static_cast<size_t>(a.touch_agg[t0 + t]) * 4 * nc + kj];
         }
     }
-    // ---- block Jacobi: M_j = K_jj^{-1} via 4x4 Cholesky (one thread per row)
+    for (int e = threadIdx.x; e < n_ext; e += blockDim.x) {
+        double d3[3];
+        node_offset(a, a.ext_node[e0 + e], d3);
+        for (int t = 0; t < 3; ++t) sh.offx[e * 3 + t] = d3[t];
+        sh.tl[e] = a.ext_tl[e0 + e];
+    }
+    // ---- 4x4 diagonal blocks must be PD (reference describe_failure)
     for (int lr = threadIdx.x; lr < nrows; lr += blockDim.x) {
         const int j = r0 + lr;
         const int node = a.row_node[j];
-        double d3[3];
-        node_offset(a, node, d3);
-        for (int t = 0; t < 3; ++t) sh.off[lr * 3 + t] = d3[t];
         int dpos = -1;
         for (int b = a.row_ptr[j]; b < a.row_ptr[j + 1]; ++b)
             if (a.col[b] == node) dpos = b;
@@ -583,7 +931,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
     // local memory).
     const int nel = nrows * 12;
     const int my_rc = threadIdx.x % 12, my_r = my_rc / 3, my_c = my_rc % 3;
-    double xr[EPT], br[EPT], rr[EPT], zr[EPT], pr[EPT];
+    double xr[EPT], br[EPT], rr[EPT], ur[EPT], wr[EPT], pr[EPT], sr[EPT], qr[EPT], zv[EPT];
     int el_row[EPT], el_b0[EPT], el_b1[EPT];  // row, block range in the CTA's K
     size_t el_g[EPT];
 #pragma unroll
@@ -597,13 +945,9 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + my_rc;
         xr[k] = live ? a.X[el_g[k]] : 0.0;
         br[k] = live ? a.B[el_g[k]] : 0.0;
-        pr[k] = zr[k] = rr[k] = 0.0;
+        rr[k] = ur[k] = wr[k] = pr[k] = sr[k] = qr[k] = zv[k] = 0.0;
     }
 
-    const int e0 = a.ext_off[cta], n_ext = a.ext_off[cta + 1] - e0;
-    // stage the halo rows of v (global, written by other CTAs before the last
-    // grid barrier) into shared memory next to the own rows: one coalesced
-    // round of L2 loads instead of a latency-bound gather per K block
     // the thread's first kHaloRegs halo elements: global offsets resolved once,
     // so a fill is kHaloRegs independent L2 loads (one round trip)
     constexpr int kHaloRegs = 4;
@@ -613,10 +957,14 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         const int t = nrows * 12 + threadIdx.x + k * blockDim.x;
         hoff[k] = t < n_ext * 12 ? a.ext_node[e0 + t / 12] * 12 + t % 12 : -1;
     }
-    auto fill_halo = [&](const double* __restrict__ v) {
+    // halo rows of v (other CTAs' rows, published before the last grid
+    // barrier) -> ext; with `totals`, the iteration's grid totals and
+    // aggregate sums are loaded in the same L2 round trip
+    auto exchange = [&](const double* __restrict__ v, bool totals) {
         double hv[kHaloRegs];
 #pragma unroll
         for (int k = 0; k < kHaloRegs; ++k) hv[k] = hoff[k] >= 0 ? __ldcg(v + hoff[k]) : 0.0;
+        if (totals) iter_totals(a, a.part_a, G, sh.bcast, sh.ptq);
         for (int t = nrows * 12 + threadIdx.x + kHaloRegs * blockDim.x; t < n_ext * 12; t += blockDim.x)
             sh.ext[t] = __ldcg(v + static_cast<size_t>(a.ext_node[e0 + t / 12]) * 12 + t % 12);
 #pragma unroll
@@ -664,9 +1012,9 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
         if (my_r < 3) {
             ps[my_r] += v;
         } else {
-            ps[0] += sh.off[lr * 3 + 0] * v;
-            ps[1] += sh.off[lr * 3 + 1] * v;
-            ps[2] += sh.off[lr * 3 + 2] * v;
+            ps[0] += sh.offx[lr * 3 + 0] * v;
+            ps[1] += sh.offx[lr * 3 + 1] * v;
+            ps[2] += sh.offx[lr * 3 + 2] * v;
             ps[3] += v;
         }
     };
@@ -675,136 +1023,14 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
 #pragma unroll
         for (int j = 0; j < kQ; ++j) vals[j] = 0.0;
     };
-    // slot base + c gets v for the own column only (compile-time base)
-    auto put_col = [&](int base, double v) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) vals[base + c] = c == my_c ? v : 0.0;
-    };
     auto put_psi = [&](int base, const double ps[4]) {
 #pragma unroll
         for (int m = 0; m < 4; ++m)
 #pragma unroll
             for (int c = 0; c < 3; ++c) vals[base + m * 3 + c] = c == my_c ? ps[m] : 0.0;
     };
-    // z = M_sub r + Psi y_own with y_own = K0inv[own aggregate rows] rho: the
-    // last warp computes y while the others apply the subdomain inverses
-    auto precond = [&]() {
-#pragma unroll
-        for (int k = 0; k < EPT; ++k)
-            if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = rr[k];
-        __syncthreads();
-        const int wlast = (blockDim.x >> 5) - 1;
-        if (a.use_coarse && (threadIdx.x >> 5) == wlast) {
-            const int lane = threadIdx.x & 31;
-            double acc[12];
-#pragma unroll
-            for (int o = 0; o < 12; ++o) acc[o] = 0.0;
-            for (int j = lane; j < nc; j += 32) {
-                const double r0 = sh.rho[j * 3], r1 = sh.rho[j * 3 + 1], r2 = sh.rho[j * 3 + 2];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const double ci = sh.cinv[k * nc + j];
-                    acc[3 * k] += ci * r0;
-                    acc[3 * k + 1] += ci * r1;
-                    acc[3 * k + 2] += ci * r2;
-                }
-            }
-#pragma unroll
-            for (int o = 0; o < 12; ++o) acc[o] = warp_sum(acc[o]);
-            if (lane == 0)
-#pragma unroll
-                for (int o = 0; o < 12; ++o) sh.y[o] = acc[o];
-        } else {
-            // zz = M_sub r: 4 threads per scalar row i split the chunk's
-            // columns, butterfly-combined in a fixed order
-            const int nthr = a.use_coarse ? wlast * 32 : static_cast<int>(blockDim.x);
-            for (int t = threadIdx.x; t < 16 * nrows; t += nthr) {
-                const int i = t >> 2, q = t & 3, lr = i >> 2;
-                const int ch = sh.rchunk[lr], st = sh.cstart[ch];
-                const int nk = 4 * (sh.cstart[ch + 1] - st);
-                const double* m = sh.Minv + ch * sub_msz + static_cast<size_t>(i - 4 * st) * sub_ld;
-                const double* rv = sh.rex + 12 * st;
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
-                int j = q;
-                for (; j + 4 < nk; j += 8) {
-                    const double mj = m[j], mk = m[j + 4];
-                    a0 = fma(mj, rv[3 * j], a0);
-                    b0 = fma(mk, rv[3 * j + 12], b0);
-                    a1 = fma(mj, rv[3 * j + 1], a1);
-                    b1 = fma(mk, rv[3 * j + 13], b1);
-                    a2 = fma(mj, rv[3 * j + 2], a2);
-                    b2 = fma(mk, rv[3 * j + 14], b2);
-                }
-                if (j < nk) {
-                    const double mj = m[j];
-                    a0 = fma(mj, rv[3 * j], a0);
-                    a1 = fma(mj, rv[3 * j + 1], a1);
-                    a2 = fma(mj, rv[3 * j + 2], a2);
-                }
-                a0 += b0;
-                a1 += b1;
-                a2 += b2;
-                const unsigned grp = 0xFu << (threadIdx.x & 28);
-                a0 += __shfl_xor_sync(grp, a0, 1);
-                a1 += __shfl_xor_sync(grp, a1, 1);
-                a2 += __shfl_xor_sync(grp, a2, 1);
-                a0 += __shfl_xor_sync(grp, a0, 2);
-                a1 += __shfl_xor_sync(grp, a1, 2);
-                a2 += __shfl_xor_sync(grp, a2, 2);
-                if (q == 0) {
-                    sh.zz[3 * i] = a0;
-                    sh.zz[3 * i + 1] = a1;
-                    sh.zz[3 * i + 2] = a2;
-                }
-            }
-        }
-        __syncthreads();
-        // z = zz + Psi y; own rows of the SpMV operand (ext) are written here:
-        // ext is next read after the halo barrier
-#pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-            if (el_row[k] < 0) {
-                zr[k] = 0.0;
-                continue;
-            }
-            const int lr = el_row[k];
-            double z = sh.zz[lr * 12 + my_rc];
-            if (a.use_coarse) {
-                if (my_r < 3) z += sh.y[my_r * 3 + my_c];
-                else
-                    z += sh.off[lr * 3] * sh.y[my_c] + sh.off[lr * 3 + 1] * sh.y[3 + my_c] +
-                         sh.off[lr * 3 + 2] * sh.y[6 + my_c] + sh.y[9 + my_c];
-            }
-            zr[k] = z;
-            __stcg(a.Z + el_g[k], z);
-            sh.ext[lr * 12 + my_rc] = z;
-        }
-    };
-
-    probe(13);  // Gauss-Jordan
-    grid.sync();  // fail flags visible
-    probe(14);
-    if (__ldcg(&a.status->fail_node) != 0x7fffffff) return;
-
-    // Chronopoulos-Gear PCG: one global reduction per iteration. With u = M r
-    // and w = K u, gamma = (r,u) and delta = (w,u) give
-    //   beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev),
-    //   p = u + beta p, s = w + beta s (= K p), x += alpha p, r -= alpha s,
-    // and the coarse residual rho = Psi^T r follows rho -= alpha sigma with
-    // sigma = Psi^T s = Psi^T w + beta sigma (Psi^T w rides on the same
-    // reduction). Per iteration: SpMV + partials, grid barrier (reduction),
-    // local updates + preconditioner, grid barrier (halo of u).
-    int it = 0, restarts = 0;
-    double bmax = 0.0, tol = 0.0, bar = 0.0;
-    double gam[3] = {0, 0, 0}, al_prev[3] = {1, 1, 1};
-    bool first = true;
-    bool need_init = true;
-    int status_code = 0;  // 1 converged, 2 indefinite, 3 max iter
-    double wr[EPT], sr[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) wr[k] = sr[k] = 0.0;
     const bool prof = a.prof != nullptr && cta == 0 && threadIdx.x == 0;
-    long long tp = clock64(), acc_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64(), acc_t[16] = {0};
     const long long t_setup = tp - t_entry;
     auto mark = [&](int slot) {
         if (prof) {
@@ -813,7 +1039,129 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             tp = t;
         }
     };
-    // per-CTA work (not waiting) cycles: spmv+partials, update+precond, halo
+    // m' = M_sub v (the subdomain part of the preconditioner) for the own rows:
+    // -> ext own rows and the global exchange buffer Z. 4 threads per scalar
+    // row split the chunk's columns, butterfly-combined in a fixed order.
+    auto precond_sub = [&](const double (&v)[EPT]) {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k)
+            if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = v[k];
+        __syncthreads();
+        for (int t = threadIdx.x; t < 16 * nrows; t += blockDim.x) {
+            const int i = t >> 2, q = t & 3, lr = i >> 2;
+            const int ch = sh.rchunk[lr], st = sh.cstart[ch];
+            const int nk = 4 * (sh.cstart[ch + 1] - st);
+            const double* m = sh.Minv + ch * sub_msz + static_cast<size_t>(i - 4 * st) * sub_ld;
+            const double* rv = sh.rex + 12 * st;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+            int j = q;
+            for (; j + 4 < nk; j += 8) {
+                const double mj = m[j], mk = m[j + 4];
+                a0 = fma(mj, rv[3 * j], a0);
+                b0 = fma(mk, rv[3 * j + 12], b0);
+                a1 = fma(mj, rv[3 * j + 1], a1);
+                b1 = fma(mk, rv[3 * j + 13], b1);
+                a2 = fma(mj, rv[3 * j + 2], a2);
+                b2 = fma(mk, rv[3 * j + 14], b2);
+            }
+            if (j < nk) {
+                const double mj = m[j];
+                a0 = fma(mj, rv[3 * j], a0);
+                a1 = fma(mj, rv[3 * j + 1], a1);
+                a2 = fma(mj, rv[3 * j + 2], a2);
+            }
+            a0 += b0;
+            a1 += b1;
+            a2 += b2;
+            const unsigned grp = 0xFu << (threadIdx.x & 28);
+            a0 += __shfl_xor_sync(grp, a0, 1);
+            a1 += __shfl_xor_sync(grp, a1, 1);
+            a2 += __shfl_xor_sync(grp, a2, 1);
+            a0 += __shfl_xor_sync(grp, a0, 2);
+            a1 += __shfl_xor_sync(grp, a1, 2);
+            a2 += __shfl_xor_sync(grp, a2, 2);
+            if (q == 0) {
+                sh.zz[3 * i] = a0;
+                sh.zz[3 * i + 1] = a1;
+                sh.zz[3 * i + 2] = a2;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            if (el_row[k] < 0) continue;
+            const double z = sh.zz[el_row[k] * 12 + my_rc];
+            __stcg(a.Z + el_g[k], z);
+            sh.ext[el_row[k] * 12 + my_rc] = z;
+        }
+    };
+    // coarse part of the preconditioner on every operand row (own + halo):
+    // ext += Psi y with y = K0^-1 (Psi^T v) for the touched aggregates, from
+    // the replicated aggregate sums in ptq. 8 lanes per K0^-1 row.
+    auto coarse_add = [&]() {
+        if (!a.use_coarse) return;
+        const int g8 = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+        const int ngroups = blockDim.x >> 3;
+        for (int row0 = 0; row0 < 4 * nt; row0 += ngroups) {  // uniform trip count: full-warp shuffles
+            const int row = row0 + g8;
+            double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+            if (row < 4 * nt) {
+                const double* ci = sh.cinv + static_cast<size_t>(row) * nc;
+                for (int j = l8; j < nc; j += 8) {
+                    const double w = ci[j];
+                    c0 = fma(w, sh.ptq[3 * j], c0);
+                    c1 = fma(w, sh.ptq[3 * j + 1], c1);
+                    c2 = fma(w, sh.ptq[3 * j + 2], c2);
+                }
+            }
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+                c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+                c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+            }
+            if (l8 == 0 && row < 4 * nt) {
+                sh.yt[row * 3] = c0;
+                sh.yt[row * 3 + 1] = c1;
+                sh.yt[row * 3 + 2] = c2;
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < n_ext * 12; t += blockDim.x) {
+            const int e = t / 12, rc = t - 12 * e, r = rc / 3, c = rc - 3 * r;
+            const double* y = sh.yt + sh.tl[e] * 12;
+            const double add = r < 3 ? y[r * 3 + c]
+                                     : sh.offx[e * 3] * y[c] + sh.offx[e * 3 + 1] * y[3 + c] +
+                                           sh.offx[e * 3 + 2] * y[6 + c] + y[9 + c];
+            sh.ext[t] += add;
+        }
+        __syncthreads();
+    };
+
+    probe(13);
+    grid.sync();  // fail flags visible
+    probe(14);
+    if (__ldcg(&a.status->fail_node) != 0x7fffffff) return;
+
+    // Pipelined PCG (Ghysels & Vanroose's recurrences with the two-level
+    // preconditioner M = M_sub + Psi K0^-1 Psi^T): one grid barrier per
+    // iteration. Before barrier i every CTA has r, u = M r, w = K u for its
+    // rows; it publishes the partials of gamma = (r,u), delta = (w,u), max|r|
+    // and Psi^T w, and m' = M_sub w. After the barrier one L2 round trip brings
+    // the totals and the halo of m'; m = m' + Psi K0^-1 Psi^T w is completed
+    // locally on own and halo rows, n = K m, and
+    //   beta = gamma/gamma_prev, alpha = gamma/(delta - beta gamma/alpha_prev),
+    //   z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p,
+    //   x += alpha p, r -= alpha s, u -= alpha q, w -= alpha z.
+    int it = 0, restarts = 0;
+    double bmax = 0.0, tol = 0.0, bar = 0.0;
+    // 1/gamma and 1/alpha of the previous iteration: one division (alpha) on
+    // the critical path
+    double gam[3] = {0, 0, 0}, inv_gam[3] = {0, 0, 0}, inv_alp[3] = {1, 1, 1};
+    bool first = true;
+    bool need_init = true;
+    int status_code = 0;  // 1 converged, 2 indefinite, 3 max iter
+    // per-CTA work (not waiting) cycles: before the barrier, after it
     const bool cprof = a.cta_prof != nullptr && threadIdx.x == 0;
     long long cw[3] = {0, 0, 0}, ct = 0;
     auto cstart_t = [&]() {
@@ -825,7 +1173,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
 
     while (true) {
         if (need_init) {
-            // r = b - K x; rho = Psi^T r; max|r|, max|B|
+            // r = b - K x; u = M r; w = K u (three exchanges)
 #pragma unroll
             for (int k = 0; k < EPT; ++k)
                 if (el_row[k] >= 0) {
@@ -833,7 +1181,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                     sh.ext[el_row[k] * 12 + my_rc] = xr[k];
                 }
             grid.sync();
-            fill_halo(a.X);
+            exchange(a.X, false);
             double rmx = 0.0, bmx = 0.0, ps[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
@@ -848,9 +1196,11 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             vals[1] = bmx;
             put_psi(2, ps);
             block_partials(vals, 14, sh.red, a.part_b, 0x3u);
+            precond_sub(rr);
             grid.sync();
+            exchange(a.Z, false);
             grid_totals(a.part_b, G, sh.bcast, 2, 0x3u);
-            if (a.use_coarse) aggregate_sums(a, a.part_b, G, 2, sh.rho, 4);
+            if (a.use_coarse) aggregate_sums(a, a.part_b, G, 2, sh.ptq, 4);
             __syncthreads();
             const double rmax0 = sh.bcast[0];
             bmax = sh.bcast[1];
@@ -870,47 +1220,40 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
                 ++restarts;
                 continue;  // verify on the true residual (need_init stays set)
             }
+            coarse_add();  // ext = u on own and halo rows
 #pragma unroll
-            for (int k = 0; k < EPT; ++k) pr[k] = sr[k] = 0.0;
-            if (a.use_coarse)
-                for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) sh.sig[o] = 0.0;
+            for (int k = 0; k < EPT; ++k) {
+                ur[k] = el_row[k] >= 0 ? sh.ext[el_row[k] * 12 + my_rc] : 0.0;
+                wr[k] = spmv(k);
+                pr[k] = sr[k] = qr[k] = zv[k] = 0.0;
+            }
             first = true;
             need_init = false;
-            __syncthreads();
-            precond();  // u = M r -> Z, own ext rows
-            grid.sync();
-            fill_halo(a.Z);
+            __syncthreads();  // ext reads done before precond_sub rewrites own rows
         }
         mark(7);
         cstart_t();
-        // ---- w = K u; partials (r,u), (w,u), max|r|, Psi^T w
+        // ---- before the barrier: partials of (r,u), (w,u), max|r|, Psi^T w; m' = M_sub w
         {
             double g = 0.0, dl = 0.0, rmx = 0.0, ps[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
-                const double w = spmv(k);
-                wr[k] = w;
                 if (el_row[k] < 0) continue;
-                g += rr[k] * zr[k];
-                dl += w * zr[k];
+                g = fma(rr[k], ur[k], g);
+                dl = fma(wr[k], ur[k], dl);
                 rmx = fmax(rmx, fabs(rr[k]));
-                psi_acc(k, w, ps);
+                psi_acc(k, wr[k], ps);
             }
-            zero_vals();
-            put_col(0, g);
-            put_col(3, dl);
-            vals[6] = rmx;
-            if (a.use_coarse) put_psi(7, ps);
+            iter_partials(g, dl, rmx, ps, a.use_coarse ? 19 : 7, sh.red, a.part_a);
         }
-        cstop_t(0);
         mark(0);
-        block_partials(vals, a.use_coarse ? 19 : 7, sh.red, a.part_a, 1u << 6);
+        precond_sub(wr);
+        cstop_t(0);
         mark(1);
         grid.sync();
         mark(2);
-        grid_totals(a.part_a, G, sh.bcast, 7, 1u << 6);
-        if (a.use_coarse) aggregate_sums(a, a.part_a, G, 7, sh.ptq, 7);
-        __syncthreads();
+        cstart_t();
+        exchange(a.Z, true);
         mark(3);
         const double rmax = sh.bcast[6];
         if (rmax <= tol) {  // recursive residual converged: verify on the true residual
@@ -922,66 +1265,64 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a) {
             status_code = 3;
             break;
         }
+        mark(10);
+        // branch-free scalars for the 3 columns (no dynamic register indexing:
+        // al / bt stay in registers)
         double al[3], bt[3];
         bool indefinite = false;
+#pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double g = sh.bcast[c], d = sh.bcast[3 + c];
-            bt[c] = (first || gam[c] == 0.0) ? 0.0 : g / gam[c];
-            const double den = bt[c] == 0.0 ? d : d - bt[c] * g / al_prev[c];
-            if (g == 0.0) {
-                al[c] = 0.0;
-            } else if (!(den > 0.0) || !isfinite(den)) {
-                indefinite = true;
-                al[c] = 0.0;
-            } else {
-                al[c] = g / den;
-            }
+            bt[c] = (first || gam[c] == 0.0) ? 0.0 : g * inv_gam[c];
+            const double den = bt[c] == 0.0 ? d : d - bt[c] * g * inv_alp[c];
+            const bool bad = g != 0.0 && (!(den > 0.0) || !isfinite(den));
+            indefinite |= bad;
+            al[c] = (g == 0.0 || bad) ? 0.0 : div_nr(g, den);
             gam[c] = g;
-            if (al[c] != 0.0) al_prev[c] = al[c];
         }
         if (indefinite) {
             status_code = 2;
             break;
         }
         first = false;
-        if (a.use_coarse)
-            for (int o = threadIdx.x; o < nc * 3; o += blockDim.x) {
-                const double sg = sh.ptq[o] + bt[o % 3] * sh.sig[o];
-                sh.sig[o] = sg;
-                sh.rho[o] -= al[o % 3] * sg;
-            }
-        cstart_t();
-        // ---- p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = M r
+        mark(8);
+        coarse_add();  // ext = m on own and halo rows
+        mark(9);
         {
-            const double a_c = al[my_c], b_c = bt[my_c];
+            const double a_c = my_c == 0 ? al[0] : (my_c == 1 ? al[1] : al[2]);
+            const double b_c = my_c == 0 ? bt[0] : (my_c == 1 ? bt[1] : bt[2]);
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 if (el_row[k] < 0) continue;
-                pr[k] = fma(b_c, pr[k], zr[k]);
+                const double m = sh.ext[el_row[k] * 12 + my_rc];
+                const double n = spmv(k);
+                zv[k] = fma(b_c, zv[k], n);
+                qr[k] = fma(b_c, qr[k], m);
                 sr[k] = fma(b_c, sr[k], wr[k]);
+                pr[k] = fma(b_c, pr[k], ur[k]);
                 xr[k] = fma(a_c, pr[k], xr[k]);
                 rr[k] = fma(-a_c, sr[k], rr[k]);
+                ur[k] = fma(-a_c, qr[k], ur[k]);
+                wr[k] = fma(-a_c, zv[k], wr[k]);
             }
         }
-        __syncthreads();  // rho updated before the coarse solve
-        precond();
+        ++it;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            inv_gam[c] = gam[c] != 0.0 ? rcp_nr(gam[c]) : 0.0;
+            if (al[c] != 0.0) inv_alp[c] = rcp_nr(al[c]);
+        }
+        __syncthreads();  // ext reads done before precond_sub rewrites own rows
         cstop_t(1);
         mark(4);
-        ++it;
-        // u of the neighbours visible (a neighbour-only flag barrier was
-        // measured slower: the skew then piles up at the reduction barrier)
-        grid.sync();
-        mark(5);
-        cstart_t();
-        fill_halo(a.Z);
-        cstop_t(2);
-        mark(6);
     }
 #pragma unroll
     for (int k = 0; k < EPT; ++k)
         if (el_row[k] >= 0) a.X[el_g[k]] = xr[k];
     if (prof)
         for (int k = 0; k < 8; ++k) a.prof[k] += acc_t[k];
+    if (prof)
+        for (int k = 8; k < 16; ++k) a.prof[8 + k] += acc_t[k];
     if (prof) {
         a.prof[8] += t_setup;
         a.prof[9] += 1;
@@ -1115,9 +1456,30 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
         ext_off[g + 1] = static_cast<int>(ext_node.size());
         max_ext = std::max(max_ext, static_cast<int>(nodes_g.size()));
     }
-    const size_t fixed = 32 * kQ + kQ + 16 + 12 * static_cast<size_t>(max_rows) /* zz */ + (max_rows + 1) / 2 +
-                         12 * static_cast<size_t>(max_rows) /* rex */ + ((3 * max_rows + 1) & ~1) + 13 * kCoarseMax +
-                         12 * static_cast<size_t>(max_ext) + 2;
+    // aggregates touched by each CTA's operand rows (coarse correction on halo rows)
+    touch_off.assign(grid + 1, 0);
+    touch_agg.clear();
+    ext_tl.assign(ext_node.size(), 0);
+    max_touch = 1;
+    for (int g = 0; g < grid; ++g) {
+        std::vector<int> t;
+        for (int e = ext_off[g]; e < ext_off[g + 1]; ++e) t.push_back(node_agg[ext_node[e]]);
+        std::sort(t.begin(), t.end());
+        t.erase(std::unique(t.begin(), t.end()), t.end());
+        for (int e = ext_off[g]; e < ext_off[g + 1]; ++e)
+            ext_tl[e] = static_cast<int>(std::lower_bound(t.begin(), t.end(), node_agg[ext_node[e]]) - t.begin());
+        touch_agg.insert(touch_agg.end(), t.begin(), t.end());
+        touch_off[g + 1] = static_cast<int>(touch_agg.size());
+        max_touch = std::max(max_touch, static_cast<int>(t.size()));
+    }
+    // coarse_partial_kernel's touched-list limit; coarse_invert_kernel's register tiles
+    if (max_touch > 64 || n_agg * n_agg > 512 * 2) use_coarse = false;
+    const size_t nc = 4 * static_cast<size_t>(n_agg);
+    const size_t fixed = kRedDoubles + kQ + 12 * static_cast<size_t>(max_rows) /* zz */ +
+                         12 * static_cast<size_t>(max_rows) /* rex */ + 3 * static_cast<size_t>(max_ext) /* offx */ +
+                         (use_coarse ? 4 * max_touch * nc : 0) /* cinv */ + 12 * static_cast<size_t>(max_touch) +
+                         3 * kCoarseMax /* ptq */ + 12 * static_cast<size_t>(max_ext) /* ext */ +
+                         (max_rows + 1) / 2 /* rchunk */ + (max_ext + 1) / 2 /* tl */ + 2;
     const size_t kbytes = static_cast<size_t>(max_kb) * (16 * sizeof(double) + sizeof(int));
     k_in_smem = sizeof(double) * fixed + kbytes + 64 <= smem_limit;
     // largest subdomain chunk (rows per dense block-Jacobi inverse) that fits
@@ -1141,16 +1503,19 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
 }
 
 void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s) {
-    const size_t psmem = static_cast<size_t>(plan.max_kb) * (22 * sizeof(double) + sizeof(int)) + 64;
+    const size_t psmem = static_cast<size_t>(plan.max_kb) * (16 * sizeof(double) + 2 * sizeof(int)) + 64;
     NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(psmem)));
-    coarse_partial_kernel<<<plan.grid, kCoarseThreads, psmem, s>>>(a, w.partial);
+    PcgArgs b = a;
+    b.max_touch = plan.max_touch;
+    coarse_partial_kernel<<<plan.grid, kCoarseThreads, psmem, s>>>(b, w.partial);
     NRR_CUDA_CHECK(cudaGetLastError());
     const int nc = 4 * plan.n_agg;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(nc) * nc + 8 * nc);
+    const size_t smem = sizeof(double) * (static_cast<size_t>(nc) * nc + 6 * 16 * static_cast<size_t>(plan.n_agg) + 32) +
+                        sizeof(int) * static_cast<size_t>(plan.grid) * plan.max_touch + 16;
     NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-    coarse_invert_kernel<<<1, kCoarseThreads, smem, s>>>(a, w.partial, w.inv, plan.grid);
+    coarse_invert_kernel<<<1, kCiThreads, smem, s>>>(b, w.partial, w.inv, plan.grid);
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -1179,6 +1544,7 @@ void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
     args.agg_ctas = plan.agg_ctas;
     args.n_agg = plan.n_agg;
     args.use_coarse = plan.use_coarse ? 1 : 0;
+    args.max_touch = plan.max_touch;
     void* kargs[] = {&args};
     const void* fn = plan.ept == 1   ? reinterpret_cast<const void*>(pcg_kernel<1>)
                      : plan.ept == 2 ? reinterpret_cast<const void*>(pcg_kernel<2>)

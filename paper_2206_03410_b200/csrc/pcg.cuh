@@ -40,6 +40,9 @@ struct PcgArgs {
     const int* colx;      // nnzb: per-CTA operand row of each block's column
     const int* ext_off;   // grid+1
     const int* ext_node;  // operand rows (own rows first, then halo) -> node id
+    const int* ext_tl;    // operand rows: index of the row's aggregate in the CTA's touched list
+    const int* touch_off; // grid+1
+    const int* touch_agg; // per CTA: the aggregates its operand rows touch (ascending)
     const double* K;      // nnzb*16
     const double* B;      // 12N node-major (by node id)
     double* X;            // 12N node-major: in = warm start, out = solution
@@ -50,7 +53,7 @@ struct PcgArgs {
     const int* node_agg;  // N: aggregate of node
     const double* coarse_inv;  // n_c x n_c
     const double* sub_inv;     // grid x sub_chunks x (4 sub_rows x sub_ld): subdomain inverses
-    double* part_a;       // grid*kPcgSlots
+    double* part_a;       // kPcgSlots x round_up(grid, 8), slot-major (iteration partials)
     double* part_b;       // grid*kPcgSlots
     PcgStatus* status;
     double rtol;
@@ -58,14 +61,14 @@ struct PcgArgs {
     int max_iter;
     int max_rows, max_kb, k_in_smem, max_ext;
     int sub_rows, sub_ld, sub_chunks;  // subdomain block-Jacobi plan
-    int agg_ctas, n_agg, use_coarse;
+    int agg_ctas, n_agg, use_coarse, max_touch;
     long long* prof;  // optional clock64 per phase (CTA 0), accumulated
     long long* cta_prof;  // optional per-CTA work cycles [grid][4] (NRR_PROF)
 };
 
 struct PcgPlan {
     int nodes = 0, grid = 0, ept = 1, max_rows = 0, max_kb = 0, max_ext = 0;
-    int agg_ctas = 1, n_agg = 1;
+    int agg_ctas = 1, n_agg = 1, max_touch = 1;
     int sub_rows = 1, sub_ld = 4, sub_chunks = 1;
     bool k_in_smem = false, use_coarse = true;
     size_t smem_bytes = 0;
@@ -74,7 +77,7 @@ struct PcgPlan {
     std::vector<int> node_row;    // N: node -> solver row
     std::vector<int> node_agg;    // N
     std::vector<double> agg_center;  // n_agg*3
-    std::vector<int> colx, ext_off, ext_node;
+    std::vector<int> colx, ext_off, ext_node, ext_tl, touch_off, touch_agg;
     // partition + row order; row_nnz = blocks per node (for balance)
     void build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit);
     // smem sizing once the BSR (in solver-row order) is known

@@ -208,7 +208,7 @@ struct nrr_ctx {
 
     // ---- per-iteration state
     DevBuf<double> x, xmm, xnext, vhat, vhat2, d2, q, wa, wr, R, K, B, Z, term_part, pcg_a, pcg_b;
-    DevBuf<int> nn_idx, deg, row_begin, d_row_node, d_node_row, d_node_agg, d_colx, d_ext_off, d_ext_node;
+    DevBuf<int> nn_idx, deg, row_begin, d_row_node, d_node_row, d_node_agg, d_colx, d_ext_off, d_ext_node, d_ext_tl, d_touch_off, d_touch_agg;
     DevBuf<double> d_agg_center, coarse_part, coarse_inv, sub_inv;
     PcgPlan plan;
     ClusterPlan cplan;
@@ -590,6 +590,9 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->d_colx.upload(c->plan.colx.data(), c->plan.colx.size(), s);
         c->d_ext_off.upload(c->plan.ext_off.data(), c->plan.ext_off.size(), s);
         c->d_ext_node.upload(c->plan.ext_node.data(), c->plan.ext_node.size(), s);
+        c->d_ext_tl.upload(c->plan.ext_tl.data(), c->plan.ext_tl.size(), s);
+        c->d_touch_off.upload(c->plan.touch_off.data(), c->plan.touch_off.size(), s);
+        c->d_touch_agg.upload(c->plan.touch_agg.data(), c->plan.touch_agg.size(), s);
         c->row_begin.upload(c->plan.row_begin.data(), c->plan.row_begin.size(), s);
         c->d_row_node.upload(c->plan.row_node.data(), N, s);
         c->d_node_row.upload(c->plan.node_row.data(), N, s);
@@ -600,7 +603,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->coarse_inv.resize(nc * nc);
         c->sub_inv.resize(static_cast<size_t>(c->plan.grid) * c->plan.sub_chunks * 4 * c->plan.sub_rows *
                           c->plan.sub_ld);
-        c->pcg_a.resize(kPcgSlots * static_cast<size_t>(c->plan.grid));
+        c->pcg_a.resize(8 * kPcgSlots * static_cast<size_t>((c->plan.grid + 7) & ~7));  // kPartReplicas copies
+        c->pcg_a.zero(s);  // slot rows are padded to a multiple of 8 CTAs: the padding stays 0
         c->pcg_b.resize(kPcgSlots * static_cast<size_t>(c->plan.grid));
         d.node_row = c->d_node_row.p;
         // cluster-resident solver (opt-in) when the graph fits one cluster's shared memory
@@ -837,6 +841,9 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     a.colx = c->d_colx.p;
     a.ext_off = c->d_ext_off.p;
     a.ext_node = c->d_ext_node.p;
+    a.ext_tl = c->d_ext_tl.p;
+    a.touch_off = c->d_touch_off.p;
+    a.touch_agg = c->d_touch_agg.p;
     a.K = c->K.p;
     a.B = c->B.p;
     a.X = xout;
@@ -871,7 +878,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
         ca.max_iter = c->opt.pcg_max_iter;
         if (std::getenv("NRR_PROF")) {
             if (c->prof.n == 0) {
-                c->prof.resize(16);
+                c->prof.resize(32);
                 c->prof.zero(c->stream);
             }
             ca.prof = c->prof.p;
@@ -882,7 +889,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     }
     if (std::getenv("NRR_PROF")) {
         if (c->prof.n == 0) {
-            c->prof.resize(16);
+            c->prof.resize(32);
             c->prof.zero(c->stream);
         }
         a.prof = c->prof.p;
@@ -897,7 +904,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     // latter's inversion)
     NRR_CUDA_CHECK(cudaEventRecord(c->fork, c->stream));
     NRR_CUDA_CHECK(cudaStreamWaitEvent(c->side, c->fork, 0));
-    launch_sub_invert(c->plan, a, c->sub_inv.p, c->side);
+    launch_sub_invert(c->plan, a, c->sub_inv.p, std::getenv("NRR_SERIAL_SETUP") ? c->stream : c->side);
     NRR_CUDA_CHECK(cudaEventRecord(c->join, c->side));
     ++c->launches;
     if (c->plan.use_coarse) {
@@ -1624,11 +1631,14 @@ int nrr_debug_solver_plan(const nrr_problem_view* p, int32_t num_sms, int64_t sm
 
 int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* pcg_iters) {
     if (ctx->prof.n && std::getenv("NRR_PROF")) {
-        long long h[16];
+        long long h[32];
         cudaMemcpy(h, ctx->prof.p, sizeof(h), cudaMemcpyDeviceToHost);
         std::fprintf(stderr, "pcg phase cycles: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
                      h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
         std::fprintf(stderr, "pcg setup cycles: %lld %lld %lld %lld %lld %lld\n", h[10], h[11], h[12], h[13], h[14], h[15]);
+        std::fprintf(stderr, "pcg fine cycles: %lld %lld %lld %lld %lld %lld %lld %lld\n", h[16], h[17], h[18], h[19],
+                     h[20], h[21], h[22], h[23]);
+        std::fprintf(stderr, "gj cycles: %lld %lld %lld %lld %lld\n", h[24], h[25], h[26], h[27], h[28]);
         if (ctx->cta_prof.n) {
             std::vector<long long> cp(ctx->cta_prof.n);
             cudaMemcpy(cp.data(), ctx->cta_prof.p, sizeof(long long) * cp.size(), cudaMemcpyDeviceToHost);

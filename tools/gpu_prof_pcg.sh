@@ -1,3 +1,1 @@
-mkdir -p gpurun_out
-./tools/sync_bench > gpurun_out/sync_bench.log 2>&1
 NRR_PROF=1 timeout 120 python tools/profile_step.py --iters 10 > gpurun_out/prof.log 2>&1
