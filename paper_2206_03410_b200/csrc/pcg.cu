@@ -689,15 +689,17 @@ constexpr int kClass = kPcgThreads / 3;
 constexpr int kPartReplicas = 8;
 constexpr int kRedDoubles = 7 * kPcgThreads;
 static_assert(kRedDoubles >= 32 * kQ, "reduction scratch");
-__device__ __forceinline__ void iter_partials(double g, double dl, double rmx, const double ps[4], int nq, double* red,
-                                              double* part) {
+__device__ __forceinline__ void partials_stage(double g, double dl, double rmx, const double ps[4], double* red) {
     const int t = threadIdx.x, c = t % 3, i = t / 3;
     red[(0 * 3 + c) * kClass + i] = g;
     red[(1 * 3 + c) * kClass + i] = dl;
 #pragma unroll
     for (int m = 0; m < 4; ++m) red[((2 + m) * 3 + c) * kClass + i] = ps[m];
     red[18 * kClass + t] = rmx;
-    __syncthreads();
+}
+// after a barrier that follows partials_stage
+__device__ __forceinline__ void partials_reduce(int nq, const double* red, double* part) {
+    const int t = threadIdx.x;
     const int s = t >> 4, hl = t & 15;
     const bool mx = s == 6;
     double v = 0.0;
@@ -1042,11 +1044,14 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     // m' = M_sub v (the subdomain part of the preconditioner) for the own rows:
     // -> ext own rows and the global exchange buffer Z. 4 threads per scalar
     // row split the chunk's columns, butterfly-combined in a fixed order.
-    auto precond_sub = [&](const double (&v)[EPT]) {
+    // with_partials: the iteration partials were staged with the input; their
+    // CTA reduction shares this routine's first barrier
+    auto precond_sub = [&](const double (&v)[EPT], bool with_partials) {
 #pragma unroll
         for (int k = 0; k < EPT; ++k)
             if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = v[k];
         __syncthreads();
+        if (with_partials) partials_reduce(a.use_coarse ? 19 : 7, sh.red, a.part_a);
         for (int t = threadIdx.x; t < 16 * nrows; t += blockDim.x) {
             const int i = t >> 2, q = t & 3, lr = i >> 2;
             const int ch = sh.rchunk[lr], st = sh.cstart[ch];
@@ -1196,7 +1201,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             vals[1] = bmx;
             put_psi(2, ps);
             block_partials(vals, 14, sh.red, a.part_b, 0x3u);
-            precond_sub(rr);
+            precond_sub(rr, false);
             grid.sync();
             exchange(a.Z, false);
             grid_totals(a.part_b, G, sh.bcast, 2, 0x3u);
@@ -1244,10 +1249,10 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
                 rmx = fmax(rmx, fabs(rr[k]));
                 psi_acc(k, wr[k], ps);
             }
-            iter_partials(g, dl, rmx, ps, a.use_coarse ? 19 : 7, sh.red, a.part_a);
+            partials_stage(g, dl, rmx, ps, sh.red);
         }
         mark(0);
-        precond_sub(wr);
+        precond_sub(wr, true);
         cstop_t(0);
         mark(1);
         grid.sync();
