@@ -29,6 +29,7 @@
 #include "nn.cuh"
 #include "nrr_cuda.h"
 #include "pcg.cuh"
+#include "setup_gpu.cuh"
 #include "pcg_cluster.cuh"
 #include "comm.hpp"
 
@@ -201,6 +202,9 @@ struct nrr_ctx {
     DevBuf<double> d_src, d_infl_w, d_anchor, d_node_pos, d_pair_c;
     std::vector<double> h_anchor;  // sum_a w_a p_a per vertex (energy.hpp:150-161)
     DevBuf<double4> d_infl_f;
+    DevBuf<int> d_edge_of_blk, d_setup_flags;
+    DevBuf<long long> d_pair_off;
+    DevBuf<unsigned char> d_setup_scratch;
     DevBuf<int> d_infl_off, d_infl_node, d_pairs, d_pair_rev, d_node_pair_off, d_row_ptr, d_col, d_ub_cptr, d_cv,
         d_cea, d_ceb, d_ub_kpos, d_ub_kpos_t, d_edges, d_edge_pab, d_edge_pba, d_lm_vertex;
     DevBuf<double> d_lm_pos;
@@ -350,22 +354,19 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->src_avg = p->src_avg_edge_length;
     c->h_src.assign(p->source, p->source + 3 * static_cast<size_t>(n));
     const int sumk = n > 0 ? p->infl_offsets[n] : 0;
-    // constant per-influence f = w [v - p; 1] and the anchor sum w p (energy.hpp:150-161)
-    std::vector<double4> f(sumk);
-    std::vector<double> anchor(3 * static_cast<size_t>(n), 0.0);
+    // influence validation (the constants w [v - p; 1] and sum w p are built
+    // on the device, setup_gpu.cu); entries per vertex for the contributor lists
+    std::vector<long long> pair_off(static_cast<size_t>(n) + 1, 0);
     for (int i = 0; i < n; ++i) {
         const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
         if (k1 <= k0) throw NumericalError("source point without influencing nodes");
-        for (int k = k0; k < k1; ++k) {
-            const int a = p->infl_nodes[k];
-            if (a < 0 || a >= N) throw ConfigError("influence node index out of range");
-            const double w = p->infl_weights[k];
-            const double* pa = p->node_positions + 3 * a;
-            const double* v = p->source + 3 * i;
-            f[k] = make_double4(w * (v[0] - pa[0]), w * (v[1] - pa[1]), w * (v[2] - pa[2]), w);
-            for (int cc = 0; cc < 3; ++cc) anchor[3 * i + cc] += w * pa[cc];
-        }
+        for (int k = k0; k < k1; ++k)
+            if (p->infl_nodes[k] < 0 || p->infl_nodes[k] >= N) throw ConfigError("influence node index out of range");
+        const long long kk = k1 - k0;
+        pair_off[i + 1] = pair_off[i] + kk * (kk + 1) / 2;
     }
+    const long long entries = pair_off[n];
+    if (entries >= (1LL << 31)) throw ConfigError("assembly contributor lists exceed 2^31 entries");
     clk.lap("influence constants");
     // BSR pattern: diagonal + both halves of each edge (energy.hpp:264-279)
     std::vector<std::vector<int>> cols(N);
@@ -409,80 +410,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         edge_of_blk[find_blk(a, b)] = e;
     }
     clk.lap("bsr");
-    // contributor lists per upper block, in vertex order (the reference's
-    // program order). Vertex ranges are counted and filled by host threads;
-    // each upper block's list is the concatenation of the ranges in order,
-    // so the result does not depend on the thread count.
     const int U = N + E;
-    const int T = std::max(1, std::min<int>(8, static_cast<int>(std::thread::hardware_concurrency())));
-    std::vector<std::vector<int>> cnt_t(T, std::vector<int>(U, 0));
-    auto range = [&](int t) { return std::make_pair(static_cast<int>(static_cast<long long>(n) * t / T),
-                                                    static_cast<int>(static_cast<long long>(n) * (t + 1) / T)); };
-    std::vector<int> bad_pair(T, 0);
-    auto count_part = [&](int t) {
-        auto [i0, i1] = range(t);
-        std::vector<int>& cnt = cnt_t[t];
-        for (int i = i0; i < i1; ++i) {
-            const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
-            for (int ka = k0; ka < k1; ++ka) {
-                ++cnt[p->infl_nodes[ka]];
-                for (int kb = k0; kb < k1; ++kb) {
-                    const int a = p->infl_nodes[ka], b = p->infl_nodes[kb];
-                    if (a >= b) continue;
-                    const int blk = find_blk(a, b);
-                    if (blk < 0) {
-                        bad_pair[t] = 1;
-                        continue;
-                    }
-                    ++cnt[N + edge_of_blk[blk]];
-                }
-            }
-        }
-    };
-    auto run_parallel = [&](auto&& fn) {
-        std::vector<std::thread> th;
-        for (int t = 1; t < T; ++t) th.emplace_back(fn, t);
-        fn(0);
-        for (auto& x : th) x.join();
-    };
-    run_parallel(count_part);
-    for (int t = 0; t < T; ++t)
-        if (bad_pair[t]) throw NumericalError("assemble: co-influencing node pair is not a graph edge");
-    std::vector<int> cptr(U + 1, 0);
-    std::vector<std::vector<int>> off_t(T, std::vector<int>(U, 0));
-    for (int u = 0; u < U; ++u) {
-        int base = cptr[u];
-        for (int t = 0; t < T; ++t) {
-            off_t[t][u] = base;
-            base += cnt_t[t][u];
-        }
-        cptr[u + 1] = base;
-    }
-    std::vector<int> cv(cptr[U]), cea(cptr[U]), ceb(cptr[U]);
-    auto fill_part = [&](int t) {
-        auto [i0, i1] = range(t);
-        std::vector<int>& fill = off_t[t];
-        for (int i = i0; i < i1; ++i) {
-            const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
-            for (int ka = k0; ka < k1; ++ka) {
-                const int a = p->infl_nodes[ka];
-                int q = fill[a]++;
-                cv[q] = i;
-                cea[q] = ka;
-                ceb[q] = ka;
-                for (int kb = k0; kb < k1; ++kb) {
-                    const int b = p->infl_nodes[kb];
-                    if (a >= b) continue;
-                    const int u = N + edge_of_blk[find_blk(a, b)];
-                    q = fill[u]++;
-                    cv[q] = i;
-                    cea[q] = ka;
-                    ceb[q] = kb;
-                }
-            }
-        }
-    };
-    run_parallel(fill_part);
     clk.lap("contributors");
     std::vector<int> kpos(U), kpos_t(U), eab(E), eba(E);
     for (int j = 0; j < N; ++j) kpos[j] = kpos_t[j] = find_blk(j, j);
@@ -520,9 +448,9 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->d_infl_off.upload(p->infl_offsets, n + 1, s);
     c->d_infl_node.upload(p->infl_nodes, sumk, s);
     c->d_infl_w.upload(p->infl_weights, sumk, s);
-    c->d_infl_f.upload(f.data(), sumk, s);
-    c->d_anchor.upload(anchor.data(), anchor.size(), s);
-    c->h_anchor = anchor;
+    c->d_infl_f.resize(std::max(sumk, 1));
+    c->d_anchor.resize(std::max<size_t>(3 * static_cast<size_t>(n), 1));
+    c->h_anchor.clear();  // downloaded on demand (nrr_assemble)
     c->d_node_pos.upload(p->node_positions, 3 * static_cast<size_t>(N), s);
     c->d_pairs.upload(p->reg_pairs, 2 * static_cast<size_t>(P), s);
     c->d_pair_c.upload(p->reg_weights, P, s);
@@ -530,10 +458,39 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->d_node_pair_off.upload(npo.data(), N + 1, s);
     c->d_row_ptr.upload(c->h_row_ptr.data(), N + 1, s);
     c->d_col.upload(c->h_col.data(), nnzb, s);
-    c->d_ub_cptr.upload(cptr.data(), U + 1, s);
-    c->d_cv.upload(cv.data(), cv.size(), s);
-    c->d_cea.upload(cea.data(), cea.size(), s);
-    c->d_ceb.upload(ceb.data(), ceb.size(), s);
+    {  // contributor lists and influence constants on the device
+        c->d_node_row.upload(c->plan.node_row.data(), N, s);
+        c->d_edge_of_blk.upload(edge_of_blk.data(), nnzb, s);
+        c->d_pair_off.upload(pair_off.data(), pair_off.size(), s);
+        c->d_ub_cptr.resize(U + 1);
+        for (auto* b : {&c->d_cv, &c->d_cea, &c->d_ceb}) b->resize(std::max<long long>(entries, 1));
+        c->d_setup_flags.resize(1);
+        c->d_setup_scratch.resize(setup_gpu_scratch_bytes(entries, U));
+        SetupGpuIn in;
+        in.n = n;
+        in.N = N;
+        in.U = U;
+        in.infl_off = c->d_infl_off.p;
+        in.infl_node = c->d_infl_node.p;
+        in.infl_w = c->d_infl_w.p;
+        in.src = c->d_src.p;
+        in.node_pos = c->d_node_pos.p;
+        in.node_row = c->d_node_row.p;
+        in.row_ptr = c->d_row_ptr.p;
+        in.col = c->d_col.p;
+        in.edge_of_blk = c->d_edge_of_blk.p;
+        in.pair_off = c->d_pair_off.p;
+        SetupGpuOut out;
+        out.infl_f = c->d_infl_f.p;
+        out.anchor = c->d_anchor.p;
+        out.cptr = c->d_ub_cptr.p;
+        out.cv = c->d_cv.p;
+        out.cea = c->d_cea.p;
+        out.ceb = c->d_ceb.p;
+        out.flags = c->d_setup_flags.p;
+        build_setup_gpu(in, entries, out, c->d_setup_scratch.p, s);
+        c->launches += 4;
+    }
     c->d_ub_kpos.upload(kpos.data(), U, s);
     c->d_ub_kpos_t.upload(kpos_t.data(), U, s);
     c->d_edges.upload(p->edges, 2 * static_cast<size_t>(E), s);
@@ -595,7 +552,6 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->d_touch_agg.upload(c->plan.touch_agg.data(), c->plan.touch_agg.size(), s);
         c->row_begin.upload(c->plan.row_begin.data(), c->plan.row_begin.size(), s);
         c->d_row_node.upload(c->plan.row_node.data(), N, s);
-        c->d_node_row.upload(c->plan.node_row.data(), N, s);
         c->d_node_agg.upload(c->plan.node_agg.data(), N, s);
         c->d_agg_center.upload(c->plan.agg_center.data(), c->plan.agg_center.size(), s);
         const size_t nc = 4 * static_cast<size_t>(c->plan.n_agg);
@@ -632,6 +588,9 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     }
     NRR_CUDA_CHECK(cudaStreamSynchronize(s));
     clk.lap("pcg uploads + sync");
+    int flags = 0;
+    NRR_CUDA_CHECK(cudaMemcpy(&flags, c->d_setup_flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flags & 1) throw NumericalError("assemble: co-influencing node pair is not a graph edge");
     c->has_problem = true;
 }
 
@@ -1482,6 +1441,12 @@ int nrr_assemble(nrr_ctx* ctx, const double* corr_points, const double* w_align,
         if (cfg_for_landmarks) upload_landmarks(ctx, *cfg_for_landmarks);
         else ctx->dp.landmarks = 0;
         // the assembly consumes q = u - anchor, as the NN pass writes it
+        if (ctx->h_anchor.size() != 3 * static_cast<size_t>(n)) {
+            ctx->h_anchor.resize(3 * static_cast<size_t>(n));
+            if (n > 0)
+                NRR_CUDA_CHECK(cudaMemcpy(ctx->h_anchor.data(), ctx->d_anchor.p, sizeof(double) * 3 * n,
+                                          cudaMemcpyDeviceToHost));
+        }
         std::vector<double> q(3 * static_cast<size_t>(n));
         for (size_t k = 0; k < q.size(); ++k) q[k] = corr_points[k] - ctx->h_anchor[k];
         NRR_CUDA_CHECK(cudaMemcpyAsync(ctx->q.p, q.data(), sizeof(double) * q.size(), cudaMemcpyHostToDevice, ctx->stream));

@@ -1,3 +1,5 @@
+# host setup breakdown of the one-shot path (config 2) on the GPU box's CPU
 mkdir -p gpurun_out
-NRR_PROF_SETUP=1 timeout 300 python tools/setup_timing.py > gpurun_out/setup_timing.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+nproc > gpurun_out/setup.log; lscpu | grep -E "Model name|^CPU\(s\)|Thread" >> gpurun_out/setup.log
+NRR_PROF_SETUP=1 timeout 300 python tools/setup_timing.py >> gpurun_out/setup.log 2>&1
+timeout 300 python tools/e2e_timing.py >> gpurun_out/setup.log 2>&1
