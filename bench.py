@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--pcg-rtol", type=float, default=None, help="override the library default (1e-13)")
     ap.add_argument("--pairs", type=int, default=256, help="config 3: number of independent pairs")
+    ap.add_argument("--pair-streams", type=int, default=6, help="config 3: pairs run side by side per GPU")
     ap.add_argument("--pair-iters", type=int, default=50, help="config 3: MM iterations per pair")
     return ap.parse_args()
 
@@ -368,40 +369,102 @@ def run_b200(args, dist):
 
 def run_pairs(args, dist):
     """Config 3: independent pairs round-robin over the ranks (no
-    communication); every pair runs the fixed-count idiom for
-    --pair-iters iterations; value = all ranks' iterations / max-over-ranks
-    device time (problem generation and per-pair setup excluded; e2e includes
-    the per-pair uploads, index build and setup through the C ABI)."""
+    communication). On each GPU the rank's pairs run
+    --pair-streams at a time: one context (own stream, PCG grid capped at
+    SMs / streams CTAs) per pair, driven by that many host threads, so the
+    small per-pair solves fill the GPU side by side. Every pair runs the
+    fixed-count idiom for --pair-iters iterations. value = all ranks'
+    iterations / max-over-ranks device time of the iterate phase (CUDA events
+    around it, every context's stream drained on both sides; problem upload,
+    plan and init_parameters excluded); e2e = the same through fresh contexts
+    with host buffers (uploads, index build, plan, init, iterations,
+    downloads), wall clock."""
+    import threading
+
+    import torch
+
     from paper_2206_03410_b200 import registration as R
 
     mine = [q for q in range(args.pairs) if q % dist.world == dist.rank]
     probs = [R.make_problem(3, seed=4000 + q) for q in mine]
-    ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
-    ctx.enable_timing(True)
-    dev_ms, iters, launches0 = 0.0, 0, ctx.stats()["launches"]
-    kms = None
+    sms = torch.cuda.get_device_properties(dist.local).multi_processor_count
+    S = max(1, min(args.pair_streams, len(mine)))
+    cap = max(8, sms // S)
+
+    def prepare(p):
+        ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol, max_ctas=cap)
+        ctx.enable_timing(False)
+        ctx.set_problem(p)
+        prm = ctx.init_parameters()
+        cfg = R.solver_config(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300,
+                              i_max=args.pair_iters)
+        return ctx, cfg
+
+    def run_threads(fn):
+        th = [threading.Thread(target=fn, args=(t,)) for t in range(S)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+
+    # phase 1 (untimed): every pair resident on the device, registration begun
+    ctxs = [prepare(p) for p in probs]
+    for ctx, cfg in ctxs:
+        ctx.begin(cfg)
+    counts = [0] * S
+    launches0 = sum(c.stats()["launches"] for c, _ in ctxs)
+    errors = []
+
+    def work(t):
+        try:
+            for ctx, _ in ctxs[t::S]:
+                acc, _, _ = ctx.iterate(args.pair_iters)
+                counts[t] += acc
+        except Exception as e:  # surfaced after the join
+            errors.append(e)
+
+    torch.cuda.synchronize(dist.local)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dist.local) as clocks:
+        e0.record()
+        run_threads(work)
+        torch.cuda.synchronize(dist.local)
+        e1.record()
+        e1.synchronize()
+    if errors:
+        raise errors[0]
+    dev_ms = e0.elapsed_time(e1)
+    iters = sum(counts)
+    launches = sum(c.stats()["launches"] for c, _ in ctxs) - launches0
+    for ctx, _ in ctxs:
+        ctx.finish()
+        ctx.close()
+    # e2e: fresh contexts, host buffers through the C ABI one-shot register
+    e2e_counts = [0] * S
+
+    def work_e2e(t):
+        try:
+            for p in probs[t::S]:
+                ctx, cfg = prepare(p)
+                ctx.begin(cfg)
+                acc, _, _ = ctx.iterate(args.pair_iters)
+                ctx.finish()
+                ctx.close()
+                e2e_counts[t] += acc
+        except Exception as e:
+            errors.append(e)
+
     dist.barrier()
     t0 = time.perf_counter()
-    with ClockSampler(dist.local) as clocks:
-        for p in probs:
-            ctx.set_problem(p)
-            prm = ctx.init_parameters()
-            cfg = R.solver_config(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300,
-                                  i_max=args.pair_iters)
-            ctx.begin(cfg)
-            acc, done, ms = ctx.iterate(args.pair_iters)
-            ctx.finish()
-            dev_ms += ms
-            iters += acc
-            st = ctx.stats()["kernel_ms"]
-            kms = {k: (kms or {}).get(k, 0.0) + v for k, v in st.items()}
+    run_threads(work_e2e)
+    torch.cuda.synchronize(dist.local)
     wall = time.perf_counter() - t0
-    dist.barrier()
-    launches = ctx.stats()["launches"] - launches0
-    ctx.close()
+    if errors:
+        raise errors[0]
     max_ms = dist.max(dev_ms)
     total = dist.sum(float(iters))
-    e2e = total / dist.max(wall)
+    e2e = dist.sum(float(sum(e2e_counts))) / dist.max(wall)
     if dist.rank == 0:
         g = probs[0].graph
         line = {
@@ -411,10 +474,12 @@ def run_pairs(args, dist):
             "data": "synthetic",
             "config": {"workload": f"config 3: {args.pairs} pairs x {probs[0].n} source points (~{g.node_count} "
                                    f"nodes), {args.pair_iters} fixed-count iterations each",
-                       "parallelism": f"pairs round-robin over {dist.world} GPU(s), no communication",
+                       "parallelism": f"pairs round-robin over {dist.world} GPU(s), no communication; "
+                                      f"{S} pairs side by side per GPU (PCG grid <= {cap} CTAs each)",
+                       "l2": "not flushed: the batch (all pairs resident) exceeds L2, each pair's working set "
+                             "stays resident during its own iterations",
                        "pairs_per_s": args.pairs / (max_ms / 1e3)},
-            "kernel_ms_per_step": {k: v / max(1, iters) for k, v in (kms or {}).items()},
-            "e2e": {"value": e2e, "unit": UNIT, "seconds": wall, "note": "wall clock incl. per-pair setup"},
+            "e2e": {"value": e2e, "unit": UNIT, "seconds": wall, "note": "wall clock, fresh contexts, incl. per-pair setup"},
             "gpu_launches": launches, "clocks": clocks.result(),
         }
         print(json.dumps(line), flush=True)

@@ -102,6 +102,8 @@ typedef struct nrr_solve_options {
     double pcg_rtol;      /* default 1e-13: AA trajectories then track the reference as long as the reference tracks itself under a change of direct-solver ordering */
     int32_t pcg_max_iter; /* default 20000 */
     int32_t record_passes;/* keep per-pass records (and NN indices if nonzero==2) */
+    int32_t max_ctas;     /* PCG grid cap, 0 = one CTA per SM; set before nrr_ctx_set_problem. Several contexts
+                             driven from several host threads then run side by side (config 3 batches) */
 } nrr_solve_options;
 
 typedef struct nrr_ctx nrr_ctx;

@@ -84,7 +84,8 @@ class ReportSummary(C.Structure):
 
 
 class SolveOptions(C.Structure):
-    _fields_ = [("pcg_rtol", C.c_double), ("pcg_max_iter", C.c_int32), ("record_passes", C.c_int32)]
+    _fields_ = [("pcg_rtol", C.c_double), ("pcg_max_iter", C.c_int32), ("record_passes", C.c_int32),
+                ("max_ctas", C.c_int32)]
 
 
 _SIGS = {

@@ -3,7 +3,10 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 
 #include "errors.hpp"
 
@@ -17,6 +20,25 @@
     } while (0)
 
 namespace nrr_b200 {
+
+// Opt a kernel into the device's full dynamic shared memory, once per
+// (kernel, device). The attribute is process-global: setting it per launch to
+// the launch's own size races when several contexts launch the same kernel
+// from several host threads (config 3 batches), so it is set to the maximum.
+inline void allow_max_smem(const void* fn) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    NRR_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.insert({fn, dev}).second) return;
+    int optin = 0;
+    NRR_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    NRR_CUDA_CHECK(cudaFuncGetAttributes(&fa, fn));
+    NRR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        optin - static_cast<int>(fa.sharedSizeBytes)));
+}
 
 constexpr int kWarp = 32;
 

@@ -484,6 +484,57 @@ __global__ void __launch_bounds__(kCiThreads) coarse_invert_kernel(PcgArgs a, co
     }
 }
 
+// Larger coarse spaces (n_agg^2 > kCiThreads * kCiTiles): K0 assembled in
+// shared memory and inverted by the shared-memory blocked Gauss-Jordan.
+__global__ void __launch_bounds__(1024) coarse_invert_smem_kernel(PcgArgs a, const double* __restrict__ partial,
+                                                                   double* __restrict__ inv, int grid) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nb = a.n_agg, nc = 4 * nb, mt = a.max_touch;
+    double* A = reinterpret_cast<double*>(smem_raw);  // nc*nc
+    double* colk = A + static_cast<size_t>(nc) * nc;   // 4 * nc
+    double* rowk = colk + 4 * nc;                      // 4 * nc
+    int* touch = reinterpret_cast<int*>(rowk + 4 * nc);  // grid * mt
+    __shared__ double s_dmax, s_pb[16];
+    __shared__ int s_blocks;
+    for (int i = threadIdx.x; i < grid * mt; i += blockDim.x) {
+        const int c = i / mt, t = i - c * mt;
+        const int t0 = a.touch_off[c], nt = a.touch_off[c + 1] - t0;
+        touch[i] = t < nt ? a.touch_agg[t0 + t] : -1;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
+        const int i = o / nc, j = o - i * nc;
+        const int g = i >> 2, k = i & 3, h = j >> 2, l = j & 3;
+        const int c0 = g * a.agg_ctas, c1 = min(c0 + a.agg_ctas, grid);
+        double sum = 0.0;
+        for (int c = c0; c < c1; ++c) {
+            int t = 0;
+            while (t < mt && touch[c * mt + t] != h) ++t;
+            if (t < mt) sum += __ldcg(partial + (static_cast<size_t>(c) * mt + t) * 16 + k * 4 + l);
+        }
+        A[o] = sum;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) {
+        const int i = o / nc, j = o - i * nc;
+        if (j < i) {
+            const double v = 0.5 * (A[i * nc + j] + A[j * nc + i]);
+            A[i * nc + j] = v;
+            A[j * nc + i] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int i = 0; i < nc; ++i) m = fmax(m, fabs(A[i * nc + i]));
+        s_dmax = m;
+        s_blocks = nb;
+    }
+    __syncthreads();
+    block_gj_inverse(A, 1, &s_blocks, nc, 0, s_pb, colk, rowk, &s_dmax, 1e-12);
+    for (int o = threadIdx.x; o < nc * nc; o += blockDim.x) inv[o] = A[o];
+}
+
 // ---------------------------------------------------------------- subdomain inverses
 // CTA c (same row partition as the PCG grid): the CTA's rows are split into
 // chunks of at most sub_rows consecutive (RCB-local) nodes; M_k = exact
@@ -1430,6 +1481,8 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
     (void)smem_limit;
 }
 
+bool nc_limit_exceeded(int n_agg) { return 4 * n_agg > 160; }
+
 void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_limit) {
     max_kb = 0;
     for (int g = 0; g < grid; ++g)
@@ -1478,7 +1531,7 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
         max_touch = std::max(max_touch, static_cast<int>(t.size()));
     }
     // coarse_partial_kernel's touched-list limit; coarse_invert_kernel's register tiles
-    if (max_touch > 64 || n_agg * n_agg > 512 * 2) use_coarse = false;
+    if (max_touch > 64 || nc_limit_exceeded(n_agg)) use_coarse = false;
     const size_t nc = 4 * static_cast<size_t>(n_agg);
     const size_t fixed = kRedDoubles + kQ + 12 * static_cast<size_t>(max_rows) /* zz */ +
                          12 * static_cast<size_t>(max_rows) /* rex */ + 3 * static_cast<size_t>(max_ext) /* offx */ +
@@ -1509,8 +1562,7 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
 
 void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s) {
     const size_t psmem = static_cast<size_t>(plan.max_kb) * (16 * sizeof(double) + 2 * sizeof(int)) + 64;
-    NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(psmem)));
+    allow_max_smem(reinterpret_cast<const void*>(coarse_partial_kernel));
     PcgArgs b = a;
     b.max_touch = plan.max_touch;
     coarse_partial_kernel<<<plan.grid, kCoarseThreads, psmem, s>>>(b, w.partial);
@@ -1518,9 +1570,15 @@ void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork
     const int nc = 4 * plan.n_agg;
     const size_t smem = sizeof(double) * (static_cast<size_t>(nc) * nc + 6 * 16 * static_cast<size_t>(plan.n_agg) + 32) +
                         sizeof(int) * static_cast<size_t>(plan.grid) * plan.max_touch + 16;
-    NRR_CUDA_CHECK(cudaFuncSetAttribute(coarse_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-    coarse_invert_kernel<<<1, kCiThreads, smem, s>>>(b, w.partial, w.inv, plan.grid);
+    allow_max_smem(reinterpret_cast<const void*>(coarse_invert_kernel));
+    if (plan.n_agg * plan.n_agg <= kCiThreads * kCiTiles) {
+        coarse_invert_kernel<<<1, kCiThreads, smem, s>>>(b, w.partial, w.inv, plan.grid);
+    } else {
+        const size_t smem2 = sizeof(double) * (static_cast<size_t>(nc) * nc + 8 * nc) +
+                             sizeof(int) * static_cast<size_t>(plan.grid) * plan.max_touch + 16;
+        allow_max_smem(reinterpret_cast<const void*>(coarse_invert_smem_kernel));
+        coarse_invert_smem_kernel<<<1, 1024, smem2, s>>>(b, w.partial, w.inv, plan.grid);
+    }
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -1528,8 +1586,7 @@ void launch_sub_invert(const PcgPlan& plan, const PcgArgs& a, double* out, cudaS
     const size_t ch = plan.sub_chunks;
     const size_t smem = sizeof(double) * (ch * 4 * plan.sub_rows * plan.sub_ld + ch * 8 * plan.sub_ld + 17 * ch) +
                         sizeof(int) * (2 * ch + 2) + 16;
-    NRR_CUDA_CHECK(cudaFuncSetAttribute(sub_invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
+    allow_max_smem(reinterpret_cast<const void*>(sub_invert_kernel));
     PcgArgs b = a;
     b.sub_rows = plan.sub_rows;
     b.sub_ld = plan.sub_ld;
@@ -1555,7 +1612,7 @@ void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
                      : plan.ept == 2 ? reinterpret_cast<const void*>(pcg_kernel<2>)
                      : plan.ept == 4 ? reinterpret_cast<const void*>(pcg_kernel<4>)
                                      : reinterpret_cast<const void*>(pcg_kernel<8>);
-    NRR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem_bytes)));
+    allow_max_smem(reinterpret_cast<const void*>(fn));
     int per_sm = 0;
     NRR_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPcgThreads, plan.smem_bytes));
     if (per_sm < 1) {

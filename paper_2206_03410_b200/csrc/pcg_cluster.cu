@@ -610,7 +610,7 @@ void launch_pcg_cluster(const ClusterPlan& plan, ClusterArgs a, cudaStream_t s) 
     a.max_ext = plan.max_ext;
     a.max_ent = plan.max_ent;
     const void* fn = reinterpret_cast<const void*>(pcg_cluster_kernel);
-    NRR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem_bytes)));
+    allow_max_smem(reinterpret_cast<const void*>(fn));
     NRR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.CS);

@@ -182,7 +182,7 @@ struct nrr_ctx {
     cudaEvent_t fork = nullptr, join = nullptr;
     int num_sms = 0;
     size_t smem_optin = 0;
-    nrr_solve_options opt{1e-13, 20000, 0};
+    nrr_solve_options opt{1e-13, 20000, 0, 0};
     int64_t launches = 0;
     bool timing = false;
 
@@ -385,7 +385,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     }
     // solver row order: RCB subdomains, one per CTA (pcg.cu)
     clk.lap("pattern");
-    if (N > 0) c->plan.build(p->node_positions, deg.data(), N, c->num_sms, c->smem_optin);
+    const int sms = c->opt.max_ctas > 0 ? std::min(c->opt.max_ctas, c->num_sms) : c->num_sms;
+    if (N > 0) c->plan.build(p->node_positions, deg.data(), N, sms, c->smem_optin);
     clk.lap("rcb plan");
     c->h_row_ptr.assign(N + 1, 0);
     c->h_col.clear();
@@ -1144,7 +1145,7 @@ void nrr_ctx_destroy(nrr_ctx* ctx) {
 
 int nrr_ctx_set_options(nrr_ctx* ctx, const nrr_solve_options* opt) {
     return guarded([&] {
-        if (!(opt->pcg_rtol > 0.0) || opt->pcg_max_iter < 1) throw ConfigError("invalid solve options");
+        if (!(opt->pcg_rtol > 0.0) || opt->pcg_max_iter < 1 || opt->max_ctas < 0) throw ConfigError("invalid solve options");
         ctx->opt = *opt;
     });
 }

@@ -238,15 +238,15 @@ def report_dict(summary, stages, iters, passes=None):
 class Context:
     """One nrr_ctx: all device buffers of one registration on one stream."""
 
-    def __init__(self, device=0, pcg_rtol=None, pcg_max_iter=None, record_passes=0):
+    def __init__(self, device=0, pcg_rtol=None, pcg_max_iter=None, record_passes=0, max_ctas=0):
         self.lib = capi.load()
         h = C.c_void_p()
         check(self.lib.nrr_ctx_create(device, C.byref(h)))
         self.h = h
         self.n = 0
         self.N = 0
-        if pcg_rtol is not None or pcg_max_iter is not None or record_passes:
-            self.set_options(pcg_rtol or 1e-13, pcg_max_iter or 20000, record_passes)
+        if pcg_rtol is not None or pcg_max_iter is not None or record_passes or max_ctas:
+            self.set_options(pcg_rtol or 1e-13, pcg_max_iter or 20000, record_passes, max_ctas)
 
     def close(self):
         if self.h:
@@ -259,8 +259,8 @@ class Context:
         except Exception:
             pass
 
-    def set_options(self, pcg_rtol=1e-13, pcg_max_iter=20000, record_passes=0):
-        o = capi.SolveOptions(pcg_rtol, pcg_max_iter, record_passes)
+    def set_options(self, pcg_rtol=1e-13, pcg_max_iter=20000, record_passes=0, max_ctas=0):
+        o = capi.SolveOptions(pcg_rtol, pcg_max_iter, record_passes, max_ctas)
         check(self.lib.nrr_ctx_set_options(self.h, C.byref(o)))
 
     def set_comm(self, unique_id: bytes, world: int, rank: int):

@@ -1,2 +1,5 @@
+# config 3 (batched pairs): side-by-side contexts sweep
 mkdir -p gpurun_out
-NRR_PCG=cluster timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 120 --csv --log-file gpurun_out/launches_c3.csv python tools/profile_step.py --config 3 --iters 3 --warmup 2 > gpurun_out/ncu_c3.log 2>&1
+for S in 1 6; do
+  timeout 900 python bench.py --config 3 --pairs 64 --pair-streams $S --no-cpu-baseline > gpurun_out/c3_s$S.log 2>&1
+done
