@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_kernel(DevProblem p, 
                                                                   const double* __restrict__ wr,
                                                                   const double* __restrict__ R, TermParams tp,
                                                                   double* __restrict__ K, double* __restrict__ B) {
+    if (p.skip != nullptr && *p.skip) return;
     __shared__ double s_w[kAsmWarps][32];
     __shared__ double s_fa[kAsmWarps][32][4];
     __shared__ double s_fb[kAsmWarps][32][4];
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_kernel(DevProblem p, 
 // landmarks (stage 0 only): sequential, one thread, fixed order
 __global__ void landmark_kernel(DevProblem p, TermParams tp, double* __restrict__ K, double* __restrict__ B) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (p.skip != nullptr && *p.skip) return;
     const double lw = tp.lm_weight;
     for (int l = 0; l < p.landmarks; ++l) {
         const int i = p.lm_vertex[l];
@@ -594,6 +596,12 @@ __global__ void __launch_bounds__(256) aa_combine_kernel(AADevice aa, int D, Slo
 }
 
 // ---------------------------------------------------------------- layout
+__global__ void pass_decision_kernel(const PassRecord* __restrict__ rec, double e_prev, int current_is_aa,
+                                     double lm_w, int* __restrict__ skip) {
+    const double e = __dadd_rn(rec->total, __dmul_rn(lm_w, rec->landmark));
+    *skip = (!isfinite(e) || (current_is_aa && e > e_prev)) ? 1 : 0;
+}
+
 __global__ void col_to_node_kernel(const double* __restrict__ in, double* __restrict__ out, int N) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 12 * N) return;
@@ -625,6 +633,12 @@ void launch_terms(const DevProblem& p, const double* x, const double* d2, const 
 void launch_energy_reduce(const DevProblem& p, const double* partials, const TermParams& tp, const double* vhat,
                           PassRecord* rec, cudaStream_t s) {
     energy_reduce_kernel<<<1, 256, 0, s>>>(p, partials, tp, vhat, rec, kTermBlocks);
+    NRR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pass_decision(const PassRecord* rec, double e_prev, int current_is_aa, double lm_w, int* skip,
+                          cudaStream_t s) {
+    pass_decision_kernel<<<1, 1, 0, s>>>(rec, e_prev, current_is_aa, lm_w, skip);
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -42,7 +42,12 @@ struct DevProblem {
     int landmarks = 0;
     const int* lm_vertex = nullptr;
     const double* lm_pos = nullptr;
+    // pass-level skip flag (device-side safeguard decision, see
+    // launch_pass_decision): nonzero = the pass reverts, assembly and solve
+    // are no-ops
+    const int* skip = nullptr;
 };
+
 
 // per-pass energy record copied to the host (pinned)
 struct PassRecord {
@@ -53,6 +58,12 @@ struct PassRecord {
     int pcg_iters, pcg_code, pcg_fail_node, pcg_restarts;
     int aa_rank, pad;
 };
+
+// Safeguard decision of the current pass on the device (solver.hpp:239):
+// skip = !finite(E) || (evaluating an AA iterate && E > E_prev), with
+// E = total + lm_w * landmark formed like the host does (no contraction).
+void launch_pass_decision(const PassRecord* rec, double e_prev, int current_is_aa, double lm_w, int* skip,
+                          cudaStream_t s);
 
 struct TermParams {
     double alpha, beta, nu_a, nu_r, lm_weight;

@@ -220,6 +220,7 @@ __device__ void block_gj_inverse(double* A, int nm, const int* blocks, int ld, s
 // (staged in shared memory), then 8 lanes per output sum the blocks of that
 // aggregate (lane-strided, butterfly-combined): deterministic, no atomics.
 __global__ void __launch_bounds__(kCoarseThreads) coarse_partial_kernel(PcgArgs a, double* __restrict__ partial) {
+    if (a.skip != nullptr && *a.skip) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int c = blockIdx.x;
     const int r0 = a.row_begin[c], r1 = a.row_begin[c + 1];
@@ -297,6 +298,7 @@ __device__ __forceinline__ void mm4(const double* a, const double* b, double* c)
 }
 __global__ void __launch_bounds__(kCiThreads) coarse_invert_kernel(PcgArgs a, const double* __restrict__ partial,
                                                                double* __restrict__ inv, int grid) {
+    if (a.skip != nullptr && *a.skip) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = a.n_agg, nc = 4 * nb, mt = a.max_touch;
     double* S = reinterpret_cast<double*>(smem_raw);             // nc*nc (symmetrisation)
@@ -488,6 +490,7 @@ __global__ void __launch_bounds__(kCiThreads) coarse_invert_kernel(PcgArgs a, co
 // shared memory and inverted by the shared-memory blocked Gauss-Jordan.
 __global__ void __launch_bounds__(1024) coarse_invert_smem_kernel(PcgArgs a, const double* __restrict__ partial,
                                                                    double* __restrict__ inv, int grid) {
+    if (a.skip != nullptr && *a.skip) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = a.n_agg, nc = 4 * nb, mt = a.max_touch;
     double* A = reinterpret_cast<double*>(smem_raw);  // nc*nc
@@ -542,6 +545,7 @@ __global__ void __launch_bounds__(1024) coarse_invert_smem_kernel(PcgArgs a, con
 // block_gj_inverse), written to out[c][k][4s x sub_ld].
 constexpr int kInvThreads = 1024;
 __global__ void __launch_bounds__(kInvThreads, 1) sub_invert_kernel(PcgArgs a, double* __restrict__ out) {
+    if (a.skip != nullptr && *a.skip) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int cta = blockIdx.x;
     const int r0 = a.row_begin[cta], r1 = a.row_begin[cta + 1], nrows = r1 - r0;
@@ -842,6 +846,7 @@ __device__ __forceinline__ void iter_totals(const PcgArgs& a, const double* __re
 
 template <int EPT>
 __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
+    if (a_param.skip != nullptr && *a_param.skip) return;  // every CTA: before any grid barrier
     cg::grid_group grid = cg::this_grid();
     // The arguments are read from shared memory inside the loop: every grid
     // barrier's gpu-scope fence invalidates the SM's caches, and a constant

@@ -56,6 +56,7 @@ struct PcgArgs {
     double* part_a;       // kPcgSlots x round_up(grid, 8), slot-major (iteration partials)
     double* part_b;       // grid*kPcgSlots
     PcgStatus* status;
+    const int* skip;      // nonzero: the pass reverts, setup kernels and the solve return at once
     double rtol;
     double true_factor;  // accept the true residual at true_factor * rtol (1+|B|max)
     int max_iter;

@@ -202,7 +202,10 @@ struct nrr_ctx {
     DevBuf<double> d_src, d_infl_w, d_anchor, d_node_pos, d_pair_c;
     std::vector<double> h_anchor;  // sum_a w_a p_a per vertex (energy.hpp:150-161)
     DevBuf<double4> d_infl_f;
-    DevBuf<int> d_edge_of_blk, d_setup_flags;
+    DevBuf<int> d_edge_of_blk, d_setup_flags, d_skip;
+    const int* pcg_skip = nullptr;  // device skip flag for the next solve (speculative pass)
+    bool nn_ready = false;          // the next pass's correspondences were queued at the end of the last one
+    cudaEvent_t eval_done = nullptr;
     DevBuf<long long> d_pair_off;
     DevBuf<unsigned char> d_setup_scratch;
     DevBuf<int> d_infl_off, d_infl_node, d_pairs, d_pair_rev, d_node_pair_off, d_row_ptr, d_col, d_ub_cptr, d_cv,
@@ -211,7 +214,7 @@ struct nrr_ctx {
     DevProblem dp{};
 
     // ---- per-iteration state
-    DevBuf<double> x, xmm, xnext, vhat, vhat2, d2, q, wa, wr, R, K, B, Z, term_part, pcg_a, pcg_b;
+    DevBuf<double> x, xmm, xmm_spec, xnext, vhat, vhat2, d2, q, wa, wr, R, K, B, Z, term_part, pcg_a, pcg_b;
     DevBuf<int> nn_idx, deg, row_begin, d_row_node, d_node_row, d_node_agg, d_colx, d_ext_off, d_ext_node, d_ext_tl, d_touch_off, d_touch_agg;
     DevBuf<double> d_agg_center, coarse_part, coarse_inv, sub_inv;
     PcgPlan plan;
@@ -258,6 +261,7 @@ struct nrr_ctx {
         if (comm) nrr_b200::nccl().comm_destroy(comm);
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
+        if (eval_done) cudaEventDestroy(eval_done);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -302,6 +306,7 @@ void nn_run(nrr_ctx* c, const double* queries, int nq, const int* prev, int* idx
     ClassTimer t(c, kNN);
     launch_nn(c->bv, queries, nq, prev, idx, d2, q, anchor, c->stream);
     ++c->launches;
+    c->nn_ready = false;
 }
 
 void set_target(nrr_ctx* c, const double* tgt, int m, bool built = false) {
@@ -529,7 +534,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     d.edge_pba = c->d_edge_pba.p;
     // state buffers
     const size_t D = 12 * static_cast<size_t>(N);
-    for (auto* b : {&c->x, &c->xmm, &c->xnext, &c->B, &c->Z}) b->resize(std::max<size_t>(D, 1));
+    for (auto* b : {&c->x, &c->xmm, &c->xmm_spec, &c->xnext, &c->B, &c->Z}) b->resize(std::max<size_t>(D, 1));
+    c->d_skip.resize(1);
     for (auto* b : {&c->vhat, &c->vhat2, &c->q}) b->resize(std::max<size_t>(3 * static_cast<size_t>(n), 1));
     c->d2.resize(std::max(n, 1));
     c->wa.resize(std::max(n, 1));
@@ -773,7 +779,8 @@ void deform_run(nrr_ctx* c, const double* x, double* out, const double* old, dou
 
 // evaluate the pass at (x, vhat): correspondences, weights, energies
 void evaluate(nrr_ctx* c, const double* x, const double* vhat, const TermParams& tp, bool warm) {
-    nn_run(c, vhat, c->n, warm ? c->nn_idx.p : nullptr, c->nn_idx.p, c->d2.p, c->q.p, c->d_anchor.p);
+    if (!(warm && c->nn_ready)) nn_run(c, vhat, c->n, warm ? c->nn_idx.p : nullptr, c->nn_idx.p, c->d2.p, c->q.p, c->d_anchor.p);
+    c->nn_ready = false;
     ClassTimer t(c, kTerms);
     NRR_CUDA_CHECK(cudaMemsetAsync(c->deg.p, 0, sizeof(int), c->stream));
     launch_terms(c->dp, x, c->d2.p, tp, c->wa.p, c->wr.p, c->R.p, c->term_part.p, c->deg.p, c->stream);
@@ -804,6 +811,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     a.ext_tl = c->d_ext_tl.p;
     a.touch_off = c->d_touch_off.p;
     a.touch_agg = c->d_touch_agg.p;
+    a.skip = c->pcg_skip;
     a.K = c->K.p;
     a.B = c->B.p;
     a.X = xout;
@@ -898,6 +906,7 @@ void run_begin(nrr_ctx* c, const nrr_solver_config& cfg_in) {
     if (c->n == 0 || c->bv.m == 0) throw NumericalError("register_surfaces: empty surface");
     RunState& r = c->run;
     r = RunState{};
+    c->nn_ready = false;
     r.t0 = std::chrono::steady_clock::now();
     r.cfg = cfg_in;
     r.lm_idx.assign(cfg_in.landmark_index, cfg_in.landmark_index + cfg_in.landmark_count);
@@ -962,9 +971,16 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     std::fill(ran, ran + nrr_ctx::kClasses, false);
     NRR_CUDA_CHECK(cudaMemsetAsync(c->d_rec.p, 0, sizeof(PassRecord), c->stream));
     // warm start from the previous pass's correspondences (init NN at the first pass)
+    const bool nn_queued = c->nn_ready;
     evaluate(c, c->x.p, c->vhat.p, tp, true);
     reduce_energies(c);
-    ran[kNN] = ran[kTerms] = true;
+    ran[kNN] = !nn_queued;  // a queued NN was timed with the previous pass
+    ran[kTerms] = true;
+    // the safeguard decision is also taken on the device, so the assembly and
+    // the solve are queued right behind the evaluation and the host's
+    // decision latency hides behind them; on a revert they return at once
+    launch_pass_decision(c->d_rec.p, r.e_prev, r.current_is_aa ? 1 : 0, r.lm_w, c->d_skip.p, c->stream);
+    ++c->launches;
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_deg.p, c->deg.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (c->opt.record_passes == 2) {
@@ -972,15 +988,27 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
         NRR_CUDA_CHECK(cudaMemcpyAsync(c->pass_nn.data() + c->pass_nn.size() - n, c->nn_idx.p, sizeof(int) * n,
                                        cudaMemcpyDeviceToHost, c->stream));
     }
-    sync(c);
+    NRR_CUDA_CHECK(cudaEventRecord(c->eval_done, c->stream));
+    c->dp.skip = c->d_skip.p;
+    assemble(c, tp);
+    if (c->comm) {  // the replicated solve needs the full K and B (north_star: allreduce before the solve)
+        allreduce(c, c->K.p, 16 * static_cast<size_t>(c->dp.nnzb), ncclFloat64, ncclSum);
+        allreduce(c, c->B.p, 12 * static_cast<size_t>(N), ncclFloat64, ncclSum);
+    }
+    c->pcg_skip = c->d_skip.p;
+    solve(c, c->x.p, c->xmm_spec.p);  // x_mm = solve(), warm start at x; kept aside until accepted
+    c->pcg_skip = nullptr;
+    c->dp.skip = nullptr;
+    NRR_CUDA_CHECK(cudaEventSynchronize(c->eval_done));
     harvest(c, ran);
+    std::fill(ran, ran + nrr_ctx::kClasses, false);
     const PassRecord e = *c->h_rec.p;
     r.degenerate_total += *c->h_deg.p;
     const double e_accept = e.total + r.lm_w * e.landmark;
     if (!std::isfinite(e_accept)) throw NumericalError("solver aborted: energy is not finite");
     const bool revert = e_accept > r.e_prev && r.current_is_aa;  // solver.hpp:239
     if (c->opt.record_passes) c->passes.push_back({e.total, r.si, revert ? 1 : 0});
-    if (revert) {  // solver.hpp:244-248
+    if (revert) {  // solver.hpp:244-248 (x_mm of the previous pass is untouched)
         NRR_CUDA_CHECK(cudaMemcpyAsync(c->x.p, c->xmm.p, sizeof(double) * D, cudaMemcpyDeviceToDevice, c->stream));
         deform_run(c, c->x.p, c->vhat.p, nullptr, nullptr);
         r.current_is_aa = false;
@@ -989,13 +1017,7 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     }
     r.e_prev = e_accept;
     nrr_iteration_record rec{e.total, e.align, e.reg, e.rot, e.landmark, 0.0, r.current_is_aa ? 1 : 0, r.si};
-    std::fill(ran, ran + nrr_ctx::kClasses, false);
-    assemble(c, tp);
-    if (c->comm) {  // the replicated solve needs the full K and B (north_star: allreduce before the solve)
-        allreduce(c, c->K.p, 16 * static_cast<size_t>(c->dp.nnzb), ncclFloat64, ncclSum);
-        allreduce(c, c->B.p, 12 * static_cast<size_t>(N), ncclFloat64, ncclSum);
-    }
-    solve(c, c->x.p, c->xmm.p);  // x_mm = solve(), warm start at x
+    std::swap(c->xmm.p, c->xmm_spec.p);
     ran[kAsm] = ran[kPcg] = true;
     aa_push_combine(c, r.win, c->xmm.p, c->x.p, nullptr, c->xnext.p, D);
     ran[kAA] = true;
@@ -1007,6 +1029,12 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     allreduce(c, &c->d_rec.p->nonfinite, 1, ncclInt32, ncclMax);
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_status.p, c->d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, c->stream));
+    // the next pass's correspondences at the new iterate (independent of the
+    // host's end-of-pass decisions; a new stage only changes the weights) are
+    // queued before the sync, so the GPU does not idle through it
+    nn_run(c, c->vhat2.p, c->n, c->nn_idx.p, c->nn_idx.p, c->d2.p, c->q.p, c->d_anchor.p);
+    c->nn_ready = true;
+    ran[kNN] = true;
     sync(c);
     harvest(c, ran);
     check_pcg(c, *c->h_status.p);
@@ -1054,6 +1082,7 @@ int run_iterate(nrr_ctx* c, int max_accepted, bool flush_l2, double* device_ms) 
 
 void run_finish(nrr_ctx* c, double* out_X, double* out_deformed) {
     RunState& r = c->run;
+    c->nn_ready = false;
     if (!r.active) throw ConfigError("no registration in progress (nrr_ctx_begin)");
     if (r.stage_open) close_stage(c);  // stopped early: record the partial stage
     const auto t2 = std::chrono::steady_clock::now();
@@ -1124,6 +1153,7 @@ int nrr_ctx_create(int device, nrr_ctx** out) {
         NRR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+        NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->eval_done, cudaEventDisableTiming));
         c->d_rec.resize(1);
         c->d_status.resize(1);
         c->deg.resize(1);

@@ -305,3 +305,55 @@ def test_register_monotone_per_stage(ctx):
         assert all(e[k] <= e[k - 1] + 1e-12 for k in range(1, len(e)))
     for a, b in zip(rep["stages"], rep["stages"][1:]):
         assert b["nu_r"] == pytest.approx(a["nu_r"] / 2)
+
+
+# --------------------------------------------------------------- batched pairs (config 3)
+def _fixed_count_run(p, iters, max_ctas=0):
+    c = R.Context(max_ctas=max_ctas)
+    try:
+        c.set_problem(p)
+        prm = c.init_parameters()
+        cfg = R.solver_config(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300,
+                              i_max=iters)
+        c.begin(cfg)
+        c.iterate(iters)
+        X, v, rep = c.finish()
+        return X, v, [it["E"] for it in rep["stages"][0]["iterations"]]
+    finally:
+        c.close()
+
+
+def test_side_by_side_contexts_match_sequential():
+    """Config 3 runs several registrations at once (one context, stream and
+    host thread each, PCG grid capped): every pair must produce bitwise the
+    result it produces alone with the same grid cap, and the energies of an
+    uncapped run within the parity band (the PCG partition differs)."""
+    import threading
+
+    probs = [R.make_problem(3, seed=4000 + q, scale=0.25) for q in range(4)]
+    alone = [_fixed_count_run(p, 12, max_ctas=24) for p in probs]
+    out = [None] * len(probs)
+
+    def work(k):
+        out[k] = _fixed_count_run(probs[k], 12, max_ctas=24)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(probs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for (Xa, va, ea), (Xb, vb, eb) in zip(alone, out):
+        assert np.array_equal(Xa, Xb) and np.array_equal(va, vb) and ea == eb
+    full = _fixed_count_run(probs[0], 12)
+    e_cap, e_full = np.array(alone[0][2]), np.array(full[2])
+    assert np.all(np.abs(e_cap - e_full) <= E_REL * np.abs(e_full))
+
+
+def test_repeat_runs_bitwise_identical():
+    """pipeline_tests.cpp:72-102 / acceptance_main.cpp:515-558: the same input
+    gives the same output, bit for bit (fixed-order reductions everywhere,
+    including the PCG's grid reductions and the GPU-built assembly plan)."""
+    p = R.make_problem(2, scale=0.05)
+    a = _fixed_count_run(p, 15)
+    b = _fixed_count_run(p, 15)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
