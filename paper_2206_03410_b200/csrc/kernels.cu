@@ -181,101 +181,147 @@ __global__ void rotations_kernel(const double* __restrict__ x, int N, double* __
 // is bitwise symmetric as the reference's mirrored program makes it).
 constexpr int kAsmWarps = 8;
 
+__device__ __forceinline__ double gcomp(const double4& g, int r) { return r == 0 ? g.x : r == 1 ? g.y : r == 2 ? g.z : g.w; }
 __device__ __forceinline__ double pair_g(const DevProblem& p, int e, int r) {
-    // g_e = c [p_i - p_j; 1]  (energy.hpp:163-173)
-    const double c = p.pair_c[e];
-    if (r == 3) return c;
-    const int i = p.pairs[2 * e], j = p.pairs[2 * e + 1];
-    return c * (p.node_pos[3 * i + r] - p.node_pos[3 * j + r]);
+    // g_e = c [p_i - p_j; 1]  (energy.hpp:163-173), precomputed per problem
+    return gcomp(p.pair_gv[e], r);
 }
 
+// Warp transpose-reduce: 32 per-lane values -> lane l holds the warp sum of
+// slot l. Every butterfly level halves the vector a lane carries (16 + 8 + 4
+// + 2 + 1 shuffles instead of 32 x 5). Fixed order: deterministic.
+__device__ __forceinline__ double transpose_reduce32(const double (&v)[32]) {
+    const int lane = threadIdx.x & 31;
+    double v16[16], v8[8], v4[4], v2[2];
+    {
+        const bool up = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const double keep = up ? v[i + 16] : v[i], send = up ? v[i] : v[i + 16];
+            v16[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+    }
+    {
+        const bool up = lane & 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double keep = up ? v16[i + 8] : v16[i], send = up ? v16[i] : v16[i + 8];
+            v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+    }
+    {
+        const bool up = lane & 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double keep = up ? v8[i + 4] : v8[i], send = up ? v8[i] : v8[i + 4];
+            v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+    }
+    {
+        const bool up = lane & 2;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double keep = up ? v4[i + 2] : v4[i], send = up ? v4[i] : v4[i + 2];
+            v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+    }
+    const bool up = lane & 1;
+    const double keep = up ? v2[1] : v2[0], send = up ? v2[0] : v2[1];
+    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+}
+
+// One warp per upper 4x4 block u of K (diagonal block of node u < N, or the
+// (a,b) block of edge u - N) and, for diagonal blocks, the node's 4x3 rows of
+// B (energy.hpp:182-228). Lane l accumulates the products of contributors
+// l, l+32, ... (and, on diagonal blocks, of the node's directed pair l) into
+// 28 slots (K[r][s] at 4r+s, B[r][s] at 16+3r+s); one transpose-reduce then
+// leaves slot l's total in lane l. Fixed order: deterministic; both mirrored
+// halves of an edge block are written from the same value (K bitwise
+// symmetric, robust_energy_tests.cpp:185-196).
 __global__ void __launch_bounds__(kAsmWarps * 32) assemble_kernel(DevProblem p, const double* __restrict__ wa,
                                                                   const double* __restrict__ q,
                                                                   const double* __restrict__ wr,
                                                                   const double* __restrict__ R, TermParams tp,
                                                                   double* __restrict__ K, double* __restrict__ B) {
     if (p.skip != nullptr && *p.skip) return;
-    __shared__ double s_w[kAsmWarps][32];
-    __shared__ double s_fa[kAsmWarps][32][4];
-    __shared__ double s_fb[kAsmWarps][32][4];
-    __shared__ double s_q[kAsmWarps][32][3];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int u = blockIdx.x * kAsmWarps + wib;
     if (u >= p.U) return;
     const bool diag = u < p.N;
     const int cb = p.ub_cptr[u], ce = p.ub_cptr[u + 1];
-    // lane roles
-    const bool kl = lane < 16;
-    const bool bl = diag && lane >= 16 && lane < 28;
-    const int r = kl ? (lane >> 2) : (lane - 16) / 3;
-    const int s = kl ? (lane & 3) : (lane - 16) % 3;
-    double acc = 0.0;
-    for (int base = cb; base < ce; base += 32) {
-        const int t = base + lane;
-        if (t < ce) {
-            const int v = p.c_v[t];
-            const double4 fa = p.infl_f[p.c_ea[t]];
-            s_w[wib][lane] = wa[v];
-            s_fa[wib][lane][0] = fa.x;
-            s_fa[wib][lane][1] = fa.y;
-            s_fa[wib][lane][2] = fa.z;
-            s_fa[wib][lane][3] = fa.w;
-            if (diag) {
-                s_q[wib][lane][0] = q[3 * v];
-                s_q[wib][lane][1] = q[3 * v + 1];
-                s_q[wib][lane][2] = q[3 * v + 2];
-            } else {
-                const double4 fb = p.infl_f[p.c_eb[t]];
-                s_fb[wib][lane][0] = fb.x;
-                s_fb[wib][lane][1] = fb.y;
-                s_fb[wib][lane][2] = fb.z;
-                s_fb[wib][lane][3] = fb.w;
+    double v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.0;
+    for (int t = cb + lane; t < ce; t += 32) {
+        const int vtx = p.c_v[t];
+        const double4 fa = p.infl_f[p.c_ea[t]];
+        const double w = wa[vtx];
+        const double a4[4] = {fa.x, fa.y, fa.z, fa.w};
+        if (diag) {
+            const double q3[3] = {q[3 * vtx], q[3 * vtx + 1], q[3 * vtx + 2]};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[4 * r + c] += w * (a4[r] * a4[c]);
+                const double wr_ = w * a4[r];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) v[16 + 3 * r + c] += wr_ * q3[c];
             }
+        } else {
+            const double4 fb = p.infl_f[p.c_eb[t]];
+            const double b4[4] = {fb.x, fb.y, fb.z, fb.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[4 * r + c] += w * (a4[r] * b4[c]);
         }
-        __syncwarp();
-        const int cnt = min(32, ce - base);
-        if (kl) {
-            const double(*fb)[4] = diag ? s_fa[wib] : s_fb[wib];
-            for (int k = 0; k < cnt; ++k) acc += s_w[wib][k] * (s_fa[wib][k][r] * fb[k][s]);
-        } else if (bl) {
-            for (int k = 0; k < cnt; ++k) acc += (s_w[wib][k] * s_fa[wib][k][r]) * s_q[wib][k][s];
-        }
-        __syncwarp();
     }
     if (diag) {
+        // regularisation: the reverse pair (i, j) of each own pair (j, i) adds
+        // w g g^T to K_jj and w g y^T (y = g[0:3]) to B_j; the own pair adds
+        // w c^2 at (3,3) and -w c g[0:3] to B row 3 (energy.hpp:194-227)
         const int j = u;
-        // regularisation terms in the reference's pair order: pairs (i, j) with
-        // i < j, then j's own range (j, i), then pairs (i, j) with i > j
         const int pb = p.node_pair_off[j], pe = p.node_pair_off[j + 1];
-        int split = pb;
-        while (split < pe && p.pairs[2 * split + 1] < j) ++split;
-        auto rev_term = [&](int e_own) {  // pair e = (i, j) = reverse of (j, i)
-            const int e = p.pair_rev[e_own];
-            const double w = wr[e];
-            if (kl) acc += w * (pair_g(p, e, r) * pair_g(p, e, s));
-            else if (bl) acc += (w * pair_g(p, e, r)) * pair_g(p, e, s);  // y_e = g_e[0:3]
-        };
-        for (int e = pb; e < split; ++e) rev_term(e);
-        for (int e = pb; e < pe; ++e) {
-            const double c = p.pair_c[e];
-            if (kl && r == 3 && s == 3) acc += wr[e] * (c * c);
-            else if (bl && r == 3) acc += (wr[e] * -c) * pair_g(p, e, s);
+        for (int eo = pb + lane; eo < pe; eo += 32) {
+            const int er = p.pair_rev[eo];
+            const double w_r = wr[er], w_o = wr[eo];
+            const double4 g = p.pair_gv[er], go = p.pair_gv[eo];
+            const double g4[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[4 * r + c] += w_r * (g4[r] * g4[c]);
+                const double wg = w_r * g4[r];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) v[16 + 3 * r + c] += wg * g4[c];
+            }
+            v[15] += w_o * (go.w * go.w);
+            const double wc = w_o * -go.w;
+            v[25] += wc * go.x;
+            v[26] += wc * go.y;
+            v[27] += wc * go.z;
         }
-        for (int e = split; e < pe; ++e) rev_term(e);
-        if (kl) {
-            if (r == s && r < 3) acc += tp.beta;
-            K[static_cast<size_t>(p.ub_kpos[u]) * 16 + r * 4 + s] = acc;
-        } else if (bl) {
-            if (r < 3) acc += tp.beta * R[9 * j + s * 3 + r];  // B += beta R^T (energy.hpp:216-217)
-            B[12 * j + 3 * r + s] = acc;
+    }
+    double acc = transpose_reduce32(v);
+    if (diag) {
+        const int j = u;
+        if (lane < 16) {
+            const int r = lane >> 2, c = lane & 3;
+            if (r == c && r < 3) acc += tp.beta;
+            K[static_cast<size_t>(p.ub_kpos[u]) * 16 + lane] = acc;
+        } else if (lane < 28) {
+            const int r = (lane - 16) / 3, c = (lane - 16) % 3;
+            if (r < 3) acc += tp.beta * R[9 * j + c * 3 + r];  // B += beta R^T (energy.hpp:216-217)
+            B[12 * j + 3 * r + c] = acc;
         }
-    } else if (kl) {
+    } else if (lane < 16) {
+        const int r = lane >> 2, c = lane & 3;
         const int ed = u - p.N;
         const int eab = p.edge_pab[ed], eba = p.edge_pba[ed];
-        if (r == 3) acc += wr[eab] * (-p.pair_c[eab] * pair_g(p, eab, s));
-        if (s == 3) acc += wr[eba] * (pair_g(p, eba, r) * -p.pair_c[eba]);
-        K[static_cast<size_t>(p.ub_kpos[u]) * 16 + r * 4 + s] = acc;
-        K[static_cast<size_t>(p.ub_kpos_t[u]) * 16 + s * 4 + r] = acc;
+        if (r == 3) acc += wr[eab] * (-p.pair_c[eab] * pair_g(p, eab, c));
+        if (c == 3) acc += wr[eba] * (pair_g(p, eba, r) * -p.pair_c[eba]);
+        K[static_cast<size_t>(p.ub_kpos[u]) * 16 + r * 4 + c] = acc;
+        K[static_cast<size_t>(p.ub_kpos_t[u]) * 16 + c * 4 + r] = acc;
     }
 }
 

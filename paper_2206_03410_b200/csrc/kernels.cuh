@@ -25,6 +25,7 @@ struct DevProblem {
     const int* pairs = nullptr;        // P*2 (i, j)
     const double* pair_c = nullptr;    // P
     const int* pair_rev = nullptr;     // P: index of (j, i)
+    const double4* pair_gv = nullptr;  // P: g_e = c [p_i - p_j; 1] (energy.hpp:163-173), fixed per problem
     const int* node_pair_off = nullptr;  // N+1: pairs with i == j, ascending j
     const int* row_ptr = nullptr;      // N+1 BSR over solver rows (pcg.cu order)
     const int* col = nullptr;          // nnzb (node ids)

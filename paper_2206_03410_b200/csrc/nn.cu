@@ -152,11 +152,13 @@ __device__ __forceinline__ double exact_d2(const double* t, double qx, double qy
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-__device__ __forceinline__ float box_dist(const float4& l, const float4& h, float qx, float qy, float qz) {
+// squared FP32 distance from the query to a box (compared with thr^2: no
+// square root on the traversal path)
+__device__ __forceinline__ float box_dist2(const float4& l, const float4& h, float qx, float qy, float qz) {
     const float dx = fmaxf(fmaxf(l.x - qx, qx - h.x), 0.f);
     const float dy = fmaxf(fmaxf(l.y - qy, qy - h.y), 0.f);
     const float dz = fmaxf(fmaxf(l.z - qz, qz - h.z), 0.f);
-    return sqrtf(dx * dx + dy * dy + dz * dz);
+    return dx * dx + dy * dy + dz * dz;
 }
 
 __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __restrict__ queries, int nq,
@@ -193,19 +195,20 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
     int sp = 0;
     if (lane == 0) {
         sn[0] = ((bv.levels) << 27);  // virtual root above the top level
-        sd[0] = 0.f;
+        sd[0] = 0.f;  // squared box distances on the stack
     }
     sp = 1;
     __syncwarp(gmask);
     // prune radius: FP32 sqrt of the FP64 best, inflated by the rounding
     // margin; refreshed only when the best changes
     float thr = static_cast<float>(sqrt(best_d2)) * 1.000001f + delta;  // inf stays inf
+    float thr2 = thr * thr;
     while (sp > 0) {
         --sp;
         const int code = sn[sp];
-        const float bdist = sd[sp];
+        const float bdist2 = sd[sp];
         __syncwarp(gmask);
-        if (bdist > thr) continue;
+        if (bdist2 > thr2) continue;
         const int L = code >> 27, v = code & ((1 << 27) - 1);
         if (L == 0) {
             const float4 p = bv.pts[8 * v + lane];
@@ -213,9 +216,13 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             memcpy(&idx, &p.w, 4);
             const float dx = p.x - fx, dy = p.y - fy, dz = p.z - fz;
             const float d2f = dx * dx + dy * dy + dz * dz;
+            const bool cand = idx >= 0 && d2f <= thr2;
+            // most leaves reached with the warm-start bound hold no candidate:
+            // skip the FP64 re-rank and the group reduction
+            if (((__ballot_sync(gmask, cand) >> gshift) & 0xFFu) == 0u) continue;
             double my_d2 = INFINITY;
             int my_i = 0x7fffffff;
-            if (idx >= 0 && d2f <= thr * thr) {
+            if (cand) {
                 my_d2 = exact_d2(bv.tgt64 + 3 * idx, qx, qy, qz);
                 my_i = idx;
             }
@@ -229,7 +236,10 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
                 }
             }
             if (my_d2 < best_d2 || (my_d2 == best_d2 && my_i < best_i)) {
-                if (my_d2 < best_d2) thr = static_cast<float>(sqrt(my_d2)) * 1.000001f + delta;
+                if (my_d2 < best_d2) {
+                    thr = static_cast<float>(sqrt(my_d2)) * 1.000001f + delta;
+                    thr2 = thr * thr;
+                }
                 best_d2 = my_d2;
                 best_i = my_i;
             }
@@ -240,9 +250,9 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             float bd = INFINITY;
             if (exists) {
                 const int b = bv.level_off[cl] + c;
-                bd = box_dist(bv.box_lo[b], bv.box_hi[b], fx, fy, fz);
+                bd = box_dist2(bv.box_lo[b], bv.box_hi[b], fx, fy, fz);
             }
-            const bool valid = exists && bd <= thr;
+            const bool valid = exists && bd <= thr2;
             const unsigned ball = (__ballot_sync(gmask, valid) >> gshift) & 0xFFu;
             const int cnt = __popc(ball);
             // children in Morton order (the warm-start bound is already tight,

@@ -201,7 +201,7 @@ struct nrr_ctx {
     std::vector<double> h_src;
     DevBuf<double> d_src, d_infl_w, d_anchor, d_node_pos, d_pair_c;
     std::vector<double> h_anchor;  // sum_a w_a p_a per vertex (energy.hpp:150-161)
-    DevBuf<double4> d_infl_f;
+    DevBuf<double4> d_infl_f, d_pair_gv;
     DevBuf<int> d_edge_of_blk, d_setup_flags, d_skip;
     const int* pcg_skip = nullptr;  // device skip flag for the next solve (speculative pass)
     bool nn_ready = false;          // the next pass's correspondences were queued at the end of the last one
@@ -461,6 +461,17 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->d_pairs.upload(p->reg_pairs, 2 * static_cast<size_t>(P), s);
     c->d_pair_c.upload(p->reg_weights, P, s);
     c->d_pair_rev.upload(rev.data(), P, s);
+    {  // g_e = c [p_i - p_j; 1] per directed pair (energy.hpp:163-173)
+        std::vector<double4> gv(std::max(P, 1));
+        for (int e = 0; e < P; ++e) {
+            const int i = p->reg_pairs[2 * e], j = p->reg_pairs[2 * e + 1];
+            const double cc = p->reg_weights[e];
+            const double* pi = p->node_positions + 3 * i;
+            const double* pj = p->node_positions + 3 * j;
+            gv[e] = make_double4(cc * (pi[0] - pj[0]), cc * (pi[1] - pj[1]), cc * (pi[2] - pj[2]), cc);
+        }
+        c->d_pair_gv.upload(gv.data(), gv.size(), s);
+    }
     c->d_node_pair_off.upload(npo.data(), N + 1, s);
     c->d_row_ptr.upload(c->h_row_ptr.data(), N + 1, s);
     c->d_col.upload(c->h_col.data(), nnzb, s);
@@ -520,6 +531,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     d.pairs = c->d_pairs.p;
     d.pair_c = c->d_pair_c.p;
     d.pair_rev = c->d_pair_rev.p;
+    d.pair_gv = c->d_pair_gv.p;
     d.node_pair_off = c->d_node_pair_off.p;
     d.row_ptr = c->d_row_ptr.p;
     d.col = c->d_col.p;
