@@ -12,7 +12,7 @@ constexpr int kPcgThreads = 384;  // multiple of 12: (row r, column c) fixed per
 constexpr int kCoarseMax = 256;
 constexpr int kPcgSlots = 32;
 constexpr int kMaxEpt = 8;       // elements per thread: up to 256 nodes per CTA   // reduction slots per CTA in part_a / part_b
-constexpr int kSubRowsMax = 16;  // nodes per dense subdomain block (64 scalar rows; measured best on cfg2)
+constexpr int kSubRowsMax = 32;  // nodes per dense subdomain block: one chunk per CTA on cfg2 (measured best once the preconditioner is reused)
 // leading dimension of a 4s x 4s subdomain inverse: >= 4s and = 4 (mod 16), so
 // the 4 threads x 4 rows of a half-warp hit 16 distinct bank pairs
 inline int sub_leading_dim(int s) {
