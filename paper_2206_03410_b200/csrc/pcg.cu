@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <numeric>
+#include <thread>
 
 #include "device_common.cuh"
 #include "pcg.cuh"
@@ -1435,8 +1436,16 @@ void rcb(RcbCtx& ctx, int lo, int hi, int g0, int g1) {
     // keep at least one node per leaf on each side when possible
     cut = std::max(cut, lo + (gm - g0));
     cut = std::min(cut, hi - (g1 - gm));
-    rcb(ctx, lo, cut, g0, gm);
-    rcb(ctx, cut, hi, gm, g1);
+    // the two halves touch disjoint ranges of ids / leaf_begin: the top levels
+    // run on separate host threads (same result as the serial recursion)
+    if (hi - lo > 2048 && g1 - g0 >= 16) {
+        std::thread left([&] { rcb(ctx, lo, cut, g0, gm); });
+        rcb(ctx, cut, hi, gm, g1);
+        left.join();
+    } else {
+        rcb(ctx, lo, cut, g0, gm);
+        rcb(ctx, cut, hi, gm, g1);
+    }
 }
 
 }  // namespace

@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "device_common.cuh"
 #include "kernels.cuh"
 #include "nn.cuh"
@@ -202,6 +204,8 @@ struct nrr_ctx {
     DevBuf<double> d_src, d_infl_w, d_anchor, d_node_pos, d_pair_c;
     std::vector<double> h_anchor;  // sum_a w_a p_a per vertex (energy.hpp:150-161)
     DevBuf<double4> d_infl_f, d_pair_gv;
+    DevBuf<double> d_med_sorted;
+    DevBuf<unsigned char> d_med_tmp;
     DevBuf<int> d_edge_of_blk, d_setup_flags, d_skip;
     const int* pcg_skip = nullptr;  // device skip flag for the next solve (speculative pass)
     bool nn_ready = false;          // the next pass's correspondences were queued at the end of the last one
@@ -371,13 +375,33 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     // influence validation (the constants w [v - p; 1] and sum w p are built
     // on the device, setup_gpu.cu); entries per vertex for the contributor lists
     std::vector<long long> pair_off(static_cast<size_t>(n) + 1, 0);
-    for (int i = 0; i < n; ++i) {
-        const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
-        if (k1 <= k0) throw NumericalError("source point without influencing nodes");
-        for (int k = k0; k < k1; ++k)
-            if (p->infl_nodes[k] < 0 || p->infl_nodes[k] >= N) throw ConfigError("influence node index out of range");
-        const long long kk = k1 - k0;
-        pair_off[i + 1] = pair_off[i] + kk * (kk + 1) / 2;
+    {  // validation and per-vertex entry counts on host threads, then the prefix
+        const int T = std::max(1, std::min<int>(8, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<int> bad(T, 0);
+        auto part = [&](int t) {
+            const int i0 = static_cast<int>(static_cast<long long>(n) * t / T);
+            const int i1 = static_cast<int>(static_cast<long long>(n) * (t + 1) / T);
+            for (int i = i0; i < i1; ++i) {
+                const int k0 = p->infl_offsets[i], k1 = p->infl_offsets[i + 1];
+                if (k1 <= k0) {
+                    bad[t] |= 1;
+                    continue;
+                }
+                for (int k = k0; k < k1; ++k)
+                    if (p->infl_nodes[k] < 0 || p->infl_nodes[k] >= N) bad[t] |= 2;
+                const long long kk = k1 - k0;
+                pair_off[i + 1] = kk * (kk + 1) / 2;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; ++t) th.emplace_back(part, t);
+        part(0);
+        for (auto& x : th) x.join();
+        int b = 0;
+        for (int v : bad) b |= v;
+        if (b & 1) throw NumericalError("source point without influencing nodes");
+        if (b & 2) throw ConfigError("influence node index out of range");
+        for (int i = 0; i < n; ++i) pair_off[i + 1] += pair_off[i];
     }
     const long long entries = pair_off[n];
     if (entries >= (1LL << 31)) throw ConfigError("assembly contributor lists exceed 2^31 entries");
@@ -572,6 +596,14 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     if (N > 0) {
         c->plan.size_smem(c->h_row_ptr.data(), c->h_col.data(), c->smem_optin);
         clk.lap("pcg smem plan");
+        if (clk.on) {
+            const PcgPlan& pl = c->plan;
+            std::fprintf(stderr,
+                         "pcg plan: grid %d max_rows %d ept %d sub_rows %d chunks %d n_agg %d max_touch %d max_ext %d "
+                         "max_kb %d k_in_smem %d smem %zu coarse %d\n",
+                         pl.grid, pl.max_rows, pl.ept, pl.sub_rows, pl.sub_chunks, pl.n_agg, pl.max_touch, pl.max_ext,
+                         pl.max_kb, pl.k_in_smem ? 1 : 0, pl.smem_bytes, pl.use_coarse ? 1 : 0);
+        }
         c->d_colx.upload(c->plan.colx.data(), c->plan.colx.size(), s);
         c->d_ext_off.upload(c->plan.ext_off.data(), c->plan.ext_off.size(), s);
         c->d_ext_node.upload(c->plan.ext_node.data(), c->plan.ext_node.size(), s);
@@ -728,7 +760,7 @@ Params init_parameters(nrr_ctx* c, const nrr_solver_config& cfg) {  // solver.hp
     require_problem(c);
     const int n = c->n;
     nn_run(c, c->d_src.p, n, nullptr, c->nn_idx.p, c->d2.p, nullptr, nullptr);
-    std::vector<double> dist(n);
+    std::vector<double> dist;
     if (c->comm) {  // all ranks' distances: gather padded slices (padding = NaN, dropped)
         int mx = n;
         DevBuf<int> dm;
@@ -751,17 +783,33 @@ Params init_parameters(nrr_ctx* c, const nrr_solver_config& cfg) {  // solver.hp
         for (double v : h)
             if (!std::isnan(v)) dist.push_back(v);
         if (static_cast<int>(dist.size()) != n_total(c)) throw ConfigError("sharded vertex counts do not add up");
-    } else {
-        NRR_CUDA_CHECK(cudaMemcpyAsync(dist.data(), c->d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
-        sync(c);
     }
-    for (auto& d : dist) d = std::sqrt(d);
-    const int n_med = static_cast<int>(dist.size());
     double median = 0.0;
-    if (n_med > 0) {  // the sorted-order median (solver.hpp:92-100) by selection
-        std::nth_element(dist.begin(), dist.begin() + n_med / 2, dist.end());
-        const double hi = dist[n_med / 2];
-        median = n_med % 2 == 1 ? hi : 0.5 * (*std::max_element(dist.begin(), dist.begin() + n_med / 2) + hi);
+    if (c->comm) {
+        for (auto& d : dist) d = std::sqrt(d);
+        const int n_med = static_cast<int>(dist.size());
+        if (n_med > 0) {  // the sorted-order median (solver.hpp:92-100) by selection
+            std::nth_element(dist.begin(), dist.begin() + n_med / 2, dist.end());
+            const double hi = dist[n_med / 2];
+            median = n_med % 2 == 1 ? hi : 0.5 * (*std::max_element(dist.begin(), dist.begin() + n_med / 2) + hi);
+        }
+    } else if (n > 0) {
+        // the same median on the device: radix-sort the squared distances
+        // (sqrt is monotone, so the middle elements are the same) and read
+        // back the two middle values only
+        size_t tb = 0;
+        NRR_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, tb, static_cast<const double*>(nullptr),
+                                                      static_cast<double*>(nullptr), n));
+        c->d_med_sorted.resize(n);
+        c->d_med_tmp.resize(tb);
+        NRR_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(c->d_med_tmp.p, tb, c->d2.p, c->d_med_sorted.p, n, 0, 64,
+                                                      c->stream));
+        double mid[2] = {0.0, 0.0};
+        const int lo = n % 2 == 1 ? n / 2 : n / 2 - 1;
+        NRR_CUDA_CHECK(cudaMemcpyAsync(mid, c->d_med_sorted.p + lo, sizeof(double) * (n % 2 == 1 ? 1 : 2),
+                                       cudaMemcpyDeviceToHost, c->stream));
+        sync(c);
+        median = n % 2 == 1 ? std::sqrt(mid[0]) : 0.5 * (std::sqrt(mid[0]) + std::sqrt(mid[1]));
     }
     Params p;
     const double l_bar = c->src_avg;
