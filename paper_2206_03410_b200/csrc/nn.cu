@@ -24,6 +24,8 @@
 #include <limits>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "device_common.cuh"
 #include "nn.cuh"
 
@@ -51,7 +53,11 @@ void BvhHost::build(const double* tgt, int m_) {
             lo[c] = std::min(lo[c], v);
             hi[c] = std::max(hi[c], v);
         }
-    for (int c = 0; c < 3; ++c) center[c] = 0.5 * (lo[c] + hi[c]);
+    for (int c = 0; c < 3; ++c) {
+        center[c] = 0.5 * (lo[c] + hi[c]);
+        this->lo[c] = lo[c];
+        this->hi[c] = hi[c];
+    }
     double ext = 0;
     for (int c = 0; c < 3; ++c) ext = std::max(ext, hi[c] - lo[c]);
     half_extent = 0;
@@ -190,6 +196,63 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             best_i = p;
         }
     }
+    // ---- grid path: a warm-started query whose search ball covers at most
+    // kGridCells cells scans those cells (8 lanes round-robin over them);
+    // every point within the bound lies in one of them (cells partition space)
+    if (bv.gpts != nullptr && best_d2 < INFINITY) {
+        const float r = static_cast<float>(sqrt(best_d2)) * 1.000001f + delta;
+        const int x0 = max(0, static_cast<int>(floorf((fx - r - bv.glx) * bv.inv_h)));
+        const int x1 = min(bv.gnx - 1, static_cast<int>(floorf((fx + r - bv.glx) * bv.inv_h)));
+        const int y0 = max(0, static_cast<int>(floorf((fy - r - bv.gly) * bv.inv_h)));
+        const int y1 = min(bv.gny - 1, static_cast<int>(floorf((fy + r - bv.gly) * bv.inv_h)));
+        const int z0 = max(0, static_cast<int>(floorf((fz - r - bv.glz) * bv.inv_h)));
+        const int z1 = min(bv.gnz - 1, static_cast<int>(floorf((fz + r - bv.glz) * bv.inv_h)));
+        const int cx = x1 - x0 + 1, cy = y1 - y0 + 1, cz = z1 - z0 + 1;
+        if (cx > 0 && cy > 0 && cz > 0 && cx * cy * cz <= bv.gmax_cells) {
+            const float r2 = r * r;
+            double my_d2 = best_d2;
+            int my_i = best_i;
+            const int ncell = cx * cy * cz;
+            for (int c = lane; c < ncell; c += 8) {
+                const int iz = c % cz, t = c / cz, iy = t % cy, ix = t / cy;
+                const int cell = ((x0 + ix) * bv.gny + (y0 + iy)) * bv.gnz + (z0 + iz);
+                const int p0 = bv.cell_start[cell], p1 = bv.cell_start[cell + 1];
+                for (int k = p0; k < p1; ++k) {
+                    const float4 pt = bv.gpts[k];
+                    const float dx = pt.x - fx, dy = pt.y - fy, dz = pt.z - fz;
+                    if (dx * dx + dy * dy + dz * dz > r2) continue;
+                    int idx;
+                    memcpy(&idx, &pt.w, 4);
+                    const double d2 = exact_d2(bv.tgt64 + 3 * idx, qx, qy, qz);
+                    if (d2 < my_d2 || (d2 == my_d2 && idx < my_i)) {
+                        my_d2 = d2;
+                        my_i = idx;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(gmask, my_d2, o, 8);
+                const int oi = __shfl_xor_sync(gmask, my_i, o, 8);
+                if (od < my_d2 || (od == my_d2 && oi < my_i)) {
+                    my_d2 = od;
+                    my_i = oi;
+                }
+            }
+            if (bv.stats && lane == 0) atomicAdd(bv.stats + 3, 1ull);
+            if (lane == 0) {
+                out_idx[group] = my_i;
+                out_d2[group] = my_d2;
+                if (out_q) {
+                    const double* t = bv.tgt64 + 3 * my_i;
+                    out_q[3 * group] = t[0] - anchor[3 * group];
+                    out_q[3 * group + 1] = t[1] - anchor[3 * group + 1];
+                    out_q[3 * group + 2] = t[2] - anchor[3 * group + 2];
+                }
+            }
+            return;
+        }
+    }
     int* sn = st_node[gl];
     float* sd = st_dist[gl];
     int sp = 0;
@@ -210,6 +273,7 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
         __syncwarp(gmask);
         if (bdist2 > thr2) continue;
         const int L = code >> 27, v = code & ((1 << 27) - 1);
+        if (bv.stats && lane == 0) atomicAdd(bv.stats + (L == 0 ? 1 : 0), 1ull);
         if (L == 0) {
             const float4 p = bv.pts[8 * v + lane];
             int idx;
@@ -220,6 +284,7 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             // most leaves reached with the warm-start bound hold no candidate:
             // skip the FP64 re-rank and the group reduction
             if (((__ballot_sync(gmask, cand) >> gshift) & 0xFFu) == 0u) continue;
+            if (bv.stats && lane == 0) atomicAdd(bv.stats + 2, 1ull);
             double my_d2 = INFINITY;
             int my_i = 0x7fffffff;
             if (cand) {
@@ -267,6 +332,7 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             __syncwarp(gmask);
         }
     }
+    if (bv.stats && lane == 0) atomicAdd(bv.stats + 3, 1ull);
     if (lane == 0) {
         out_idx[group] = best_i;
         out_d2[group] = best_d2;
@@ -286,6 +352,112 @@ void launch_nn(const BvhView& bv, const double* queries, int nq, const int* prev
     if (nq <= 0) return;
     const int blocks = (nq + kGroupsPerBlock - 1) / kGroupsPerBlock;
     nn_kernel<<<blocks, kGroupsPerBlock * 8, 0, s>>>(bv, queries, nq, prev_idx, out_idx, out_d2, out_q, anchor);
+    NRR_CUDA_CHECK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- uniform grid
+namespace {
+
+__global__ void grid_cell_kernel(const double* __restrict__ t, int m, double cx, double cy, double cz, float lx,
+                                 float ly, float lz, float inv_h, int nx, int ny, int nz, int* __restrict__ key,
+                                 int* __restrict__ val, int* __restrict__ cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    // the same FP32 quantities the query path uses
+    const float px = static_cast<float>(t[3 * i] - cx), py = static_cast<float>(t[3 * i + 1] - cy),
+                pz = static_cast<float>(t[3 * i + 2] - cz);
+    const int ix = min(nx - 1, max(0, static_cast<int>(floorf((px - lx) * inv_h))));
+    const int iy = min(ny - 1, max(0, static_cast<int>(floorf((py - ly) * inv_h))));
+    const int iz = min(nz - 1, max(0, static_cast<int>(floorf((pz - lz) * inv_h))));
+    const int cell = (ix * ny + iy) * nz + iz;
+    key[i] = cell;
+    val[i] = i;
+    atomicAdd(cnt + cell, 1);
+}
+
+__global__ void grid_points_kernel(const double* __restrict__ t, int m, double cx, double cy, double cz,
+                                   const int* __restrict__ order, float4* __restrict__ gpts) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int i = order[k];
+    float4 p;
+    p.x = static_cast<float>(t[3 * i] - cx);
+    p.y = static_cast<float>(t[3 * i + 1] - cy);
+    p.z = static_cast<float>(t[3 * i + 2] - cz);
+    memcpy(&p.w, &i, 4);
+    gpts[k] = p;
+}
+
+size_t a256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+int bits_for(long long n) {
+    int b = 1;
+    while ((1LL << b) < n) ++b;
+    return b;
+}
+
+}  // namespace
+
+GridDims grid_dims(const double lo[3], const double hi[3], int m, double factor) {
+    GridDims g;
+    double ext[3], vol = 1.0, emax = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        ext[c] = hi[c] - lo[c];
+        emax = std::max(emax, ext[c]);
+    }
+    if (!(emax > 0.0) || m < 64) return g;
+    for (int c = 0; c < 3; ++c) vol *= std::max(ext[c], emax * 1e-3);
+    double h = factor * std::cbrt(vol / m);
+    for (int pass = 0; pass < 64; ++pass) {
+        const long long nx = static_cast<long long>(ext[0] / h) + 1, ny = static_cast<long long>(ext[1] / h) + 1,
+                        nz = static_cast<long long>(ext[2] / h) + 1;
+        if (nx * ny * nz <= (32LL << 20)) {
+            g.nx = static_cast<int>(nx);
+            g.ny = static_cast<int>(ny);
+            g.nz = static_cast<int>(nz);
+            g.h = h;
+            return g;
+        }
+        h *= 1.25;
+    }
+    return g;
+}
+
+size_t grid_scratch_bytes(int m, long long ncells) {
+    size_t sort_b = 0, scan_b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_b, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                    static_cast<const int*>(nullptr), static_cast<int*>(nullptr), m, 0,
+                                    bits_for(ncells));
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_b, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                  static_cast<int>(ncells + 1));
+    return 4 * a256(sizeof(int) * static_cast<size_t>(m)) + a256(sizeof(int) * static_cast<size_t>(ncells + 1)) +
+           a256(std::max(sort_b, scan_b)) + 256;
+}
+
+void build_grid(const double* tgt64, int m, const double center[3], const double lo[3], const GridDims& g,
+                float4* gpts, int* cell_start, void* scratch, cudaStream_t s) {
+    const long long ncells = static_cast<long long>(g.nx) * g.ny * g.nz;
+    char* p = static_cast<char*>(scratch);
+    const size_t eb = a256(sizeof(int) * static_cast<size_t>(m));
+    int* key = reinterpret_cast<int*>(p);
+    int* key2 = reinterpret_cast<int*>(p + eb);
+    int* val = reinterpret_cast<int*>(p + 2 * eb);
+    int* val2 = reinterpret_cast<int*>(p + 3 * eb);
+    int* cnt = reinterpret_cast<int*>(p + 4 * eb);
+    void* tmp = p + 4 * eb + a256(sizeof(int) * static_cast<size_t>(ncells + 1));
+    size_t tb = grid_scratch_bytes(m, ncells);
+    NRR_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * static_cast<size_t>(ncells + 1), s));
+    const float lx = static_cast<float>(lo[0] - center[0]), ly = static_cast<float>(lo[1] - center[1]),
+                lz = static_cast<float>(lo[2] - center[2]);
+    const float inv_h = static_cast<float>(1.0 / g.h);
+    const int blocks = (m + 255) / 256;
+    grid_cell_kernel<<<blocks, 256, 0, s>>>(tgt64, m, center[0], center[1], center[2], lx, ly, lz, inv_h, g.nx, g.ny,
+                                            g.nz, key, val, cnt);
+    NRR_CUDA_CHECK(cudaGetLastError());
+    NRR_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, val, val2, m, 0, bits_for(ncells), s));
+    tb = grid_scratch_bytes(m, ncells);
+    NRR_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, cell_start, static_cast<int>(ncells + 1), s));
+    grid_points_kernel<<<blocks, 256, 0, s>>>(tgt64, m, center[0], center[1], center[2], val2, gpts);
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -13,6 +13,7 @@ constexpr int kMaxLevels = 12;
 struct BvhHost {
     int m = 0;
     double center[3] = {0, 0, 0};
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     double half_extent = 0;
     std::vector<float4> pts;             // Morton order, padded to 8
     std::vector<float4> box_lo, box_hi;  // all levels, level 0 = leaves
@@ -32,7 +33,28 @@ struct BvhView {
     int level_cnt[kMaxLevels];
     double cx, cy, cz;
     float half_extent;
+    unsigned long long* stats;  // optional (NRR_NN_STATS): [internal visits, leaf visits, leaf hits, queries]
+    // uniform grid over the same points (warm-started queries whose search
+    // ball covers few cells skip the tree): cells of size h from (glx, gly,
+    // glz) relative to the centre, cell-major float4 points, cell_start[ncells+1]
+    const float4* gpts;
+    const int* cell_start;
+    int gnx, gny, gnz, gmax_cells;
+    float glx, gly, glz, inv_h;
 };
+
+// Grid parameters for m points in the box [lo, hi] (cell ~ half the mean
+// spacing of a surface sample; <= 32M cells). Returns false if no grid.
+struct GridDims {
+    int nx = 0, ny = 0, nz = 0;
+    double h = 0;
+};
+GridDims grid_dims(const double lo[3], const double hi[3], int m, double factor = 1.4);
+// Device grid build on `s`: targets tgt64 (m x 3, original order), centre.
+// scratch: grid_scratch_bytes(m, ncells) bytes; out: gpts (m), cell_start (ncells+1)
+size_t grid_scratch_bytes(int m, long long ncells);
+void build_grid(const double* tgt64, int m, const double center[3], const double lo[3], const GridDims& g,
+                float4* gpts, int* cell_start, void* scratch, cudaStream_t s);
 
 // out_q (optional) = target point - anchor per query (B's q_i, energy.hpp:204)
 void launch_nn(const BvhView& bv, const double* queries, int nq, const int* prev_idx, int* out_idx, double* out_d2,

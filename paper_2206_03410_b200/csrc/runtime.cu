@@ -190,7 +190,9 @@ struct nrr_ctx {
 
     // ---- target (SpatialIndex)
     BvhHost bvh;
-    DevBuf<float4> d_pts, d_lo, d_hi;
+    DevBuf<float4> d_pts, d_lo, d_hi, d_gpts;
+    DevBuf<int> d_cell_start;
+    DevBuf<unsigned char> d_grid_scratch;
     DevBuf<double> d_tgt;
     BvhView bv{};
     bool has_target = false;
@@ -205,6 +207,7 @@ struct nrr_ctx {
     std::vector<double> h_anchor;  // sum_a w_a p_a per vertex (energy.hpp:150-161)
     DevBuf<double4> d_infl_f, d_pair_gv;
     DevBuf<double> d_med_sorted;
+    DevBuf<unsigned long long> nn_stats;
     DevBuf<unsigned char> d_med_tmp;
     DevBuf<int> d_edge_of_blk, d_setup_flags, d_skip;
     const int* pcg_skip = nullptr;  // device skip flag for the next solve (speculative pass)
@@ -344,6 +347,40 @@ void set_target(nrr_ctx* c, const double* tgt, int m, bool built = false) {
     b.cy = c->bvh.center[1];
     b.cz = c->bvh.center[2];
     b.half_extent = static_cast<float>(c->bvh.half_extent);
+    b.gpts = nullptr;
+    b.cell_start = nullptr;
+    {  // uniform grid beside the BVH (warm-started queries with a small ball)
+        const char* ge = std::getenv("NRR_NN_GRID");
+        const char* gh = std::getenv("NRR_NN_GRID_H");
+        const GridDims g = (ge && std::atoi(ge) == 0) ? GridDims{}
+                                                      : grid_dims(c->bvh.lo, c->bvh.hi, m, gh ? std::atof(gh) : 1.4);
+        if (g.nx > 0) {
+            const long long ncells = static_cast<long long>(g.nx) * g.ny * g.nz;
+            c->d_gpts.resize(m);
+            c->d_cell_start.resize(static_cast<size_t>(ncells + 1));
+            c->d_grid_scratch.resize(grid_scratch_bytes(m, ncells));
+            build_grid(c->d_tgt.p, m, c->bvh.center, c->bvh.lo, g, c->d_gpts.p, c->d_cell_start.p,
+                       c->d_grid_scratch.p, c->stream);
+            c->launches += 4;
+            b.gpts = c->d_gpts.p;
+            b.cell_start = c->d_cell_start.p;
+            b.gnx = g.nx;
+            b.gny = g.ny;
+            b.gnz = g.nz;
+            b.glx = static_cast<float>(c->bvh.lo[0] - c->bvh.center[0]);
+            b.gly = static_cast<float>(c->bvh.lo[1] - c->bvh.center[1]);
+            b.glz = static_cast<float>(c->bvh.lo[2] - c->bvh.center[2]);
+            b.inv_h = static_cast<float>(1.0 / g.h);
+            const char* gc = std::getenv("NRR_NN_GRID_CELLS");
+            b.gmax_cells = gc ? std::atoi(gc) : 216;
+        }
+    }
+    b.stats = nullptr;
+    if (std::getenv("NRR_NN_STATS")) {
+        c->nn_stats.resize(4);
+        c->nn_stats.zero(c->stream);
+        b.stats = c->nn_stats.p;
+    }
     c->has_target = true;
 }
 
@@ -1739,6 +1776,12 @@ int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* 
                              ctx->plan.row_begin[arg + 1] - ctx->plan.row_begin[arg]);
             }
         }
+    }
+    if (ctx->nn_stats.n && std::getenv("NRR_NN_STATS")) {
+        unsigned long long h[4];
+        cudaMemcpy(h, ctx->nn_stats.p, sizeof(h), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "nn stats: queries %llu internal visits/query %.2f leaf visits/query %.2f leaf hits/query %.3f\n",
+                     h[3], double(h[0]) / h[3], double(h[1]) / h[3], double(h[2]) / h[3]);
     }
     if (launches) *launches = ctx->launches;
     if (kernel_ms6)
