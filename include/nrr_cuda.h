@@ -168,6 +168,11 @@ int nrr_ctx_report(nrr_ctx* ctx, nrr_report_summary* summary, nrr_stage_record* 
  * energy.hpp:28-42) for a batch of host queries; out_distance = sqrt(d2). */
 int nrr_nearest(nrr_ctx* ctx, const double* queries, int32_t q, int32_t* out_index,
                 double* out_distance);
+/* the same with a warm start: prev_index[i] (a valid target index, or -1) seeds
+ * query i's bound, as the registration loop seeds each pass with the previous
+ * pass's correspondences; the result is the same exact argmin */
+int nrr_nearest_from(nrr_ctx* ctx, const double* queries, int32_t q, const int32_t* prev_index,
+                     int32_t* out_index, double* out_distance);
 
 /* deform_points (deformation_graph.hpp:225-245) at host X */
 int nrr_deform(nrr_ctx* ctx, const double* X, double* out_points);

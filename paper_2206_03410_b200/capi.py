@@ -104,6 +104,7 @@ _SIGS = {
     "nrr_ctx_report": (C.c_int, [C.c_void_p, C.POINTER(ReportSummary), C.POINTER(StageRecord), C.c_int32,
                                  C.POINTER(IterationRecord), C.c_int32, C.POINTER(PassRecord), C.c_int32, i32p]),
     "nrr_nearest": (C.c_int, [C.c_void_p, f64p, C.c_int32, i32p, f64p]),
+    "nrr_nearest_from": (C.c_int, [C.c_void_p, f64p, C.c_int32, i32p, i32p, f64p]),
     "nrr_deform": (C.c_int, [C.c_void_p, f64p, f64p]),
     "nrr_project_rotations": (C.c_int, [C.c_void_p, f64p, C.c_int32, f64p, i32p]),
     "nrr_step": (C.c_int, [C.c_void_p, f64p, f64p, C.c_double, C.POINTER(SolverConfig), i32p, f64p, f64p,

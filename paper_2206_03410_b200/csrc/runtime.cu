@@ -1437,23 +1437,29 @@ int nrr_ctx_report(nrr_ctx* ctx, nrr_report_summary* summary, nrr_stage_record* 
     });
 }
 
-int nrr_nearest(nrr_ctx* ctx, const double* queries, int32_t q, int32_t* out_index, double* out_distance) {
+int nrr_nearest_from(nrr_ctx* ctx, const double* queries, int32_t q, const int32_t* prev_index, int32_t* out_index,
+                     double* out_distance) {
     return guarded([&] {
         NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
         require_target(ctx);
         if (q <= 0) return;
         DevBuf<double> dq, dd;
-        DevBuf<int> di;
+        DevBuf<int> di, dp;
         dq.upload(queries, 3 * static_cast<size_t>(q), ctx->stream);
         dd.resize(q);
         di.resize(q);
-        nn_run(ctx, dq.p, q, nullptr, di.p, dd.p, nullptr, nullptr);
+        if (prev_index) dp.upload(prev_index, q, ctx->stream);
+        nn_run(ctx, dq.p, q, prev_index ? dp.p : nullptr, di.p, dd.p, nullptr, nullptr);
         std::vector<double> d2(q);
         NRR_CUDA_CHECK(cudaMemcpyAsync(out_index, di.p, sizeof(int) * q, cudaMemcpyDeviceToHost, ctx->stream));
         NRR_CUDA_CHECK(cudaMemcpyAsync(d2.data(), dd.p, sizeof(double) * q, cudaMemcpyDeviceToHost, ctx->stream));
         sync(ctx);
         for (int i = 0; i < q; ++i) out_distance[i] = std::sqrt(d2[i]);  // kd_tree.hpp:128
     });
+}
+
+int nrr_nearest(nrr_ctx* ctx, const double* queries, int32_t q, int32_t* out_index, double* out_distance) {
+    return nrr_nearest_from(ctx, queries, q, nullptr, out_index, out_distance);
 }
 
 int nrr_deform(nrr_ctx* ctx, const double* X, double* out_points) {

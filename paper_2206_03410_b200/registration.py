@@ -331,11 +331,17 @@ class Context:
             rep["pass_nn"] = nn
         return rep
 
-    def nearest(self, queries):
+    def nearest(self, queries, prev=None):
+        """Exact nearest target (smallest index on ties); `prev` (target
+        indices) warm-starts the bound as the registration passes do."""
         q = f64(queries).reshape(-1, 3)
         idx = np.zeros(len(q), np.int32)
         dist = np.zeros(len(q))
-        check(self.lib.nrr_nearest(self.h, d(q), len(q), i(idx), d(dist)))
+        if prev is None:
+            check(self.lib.nrr_nearest(self.h, d(q), len(q), i(idx), d(dist)))
+        else:
+            pv = np.ascontiguousarray(prev, dtype=np.int32)
+            check(self.lib.nrr_nearest_from(self.h, d(q), len(q), i(pv), i(idx), d(dist)))
         return idx, dist
 
     def deform(self, X):

@@ -92,6 +92,56 @@ def test_nn_surface_with_holes_and_outliers(ctx):
     _nn_match(ig, dg, io, do)
 
 
+@pytest.mark.parametrize("n", [2000, 100000])
+def test_nn_warm_start_matches_exhaustive_scan(ctx, n):
+    """Warm-started queries (the registration passes' path: uniform-grid scan
+    when the bound's ball covers few cells, BVH otherwise): seeds near the
+    answer, far from it, and invalid (-1) must all give the exact argmin."""
+    rng = np.random.default_rng(77 + n)
+    pts = rng.uniform(-1, 1, (n, 3))
+    q = rng.uniform(-1.2, 1.2, (max(200, n // 10), 3))
+    ctx.set_target(pts)
+    io, do = O.nearest(pts, q)
+    seeds = [io.copy(),                                                  # the answer itself
+             (io + rng.integers(1, 5, len(io))) % n,                     # Morton-near in index only
+             rng.integers(0, n, len(io)).astype(np.int32),              # arbitrary
+             np.full(len(io), -1, np.int32)]                              # no seed
+    for prev in seeds:
+        ig, dg = ctx.nearest(q, prev=prev.astype(np.int32))
+        _nn_match(ig, dg, io, do)
+
+
+def test_nn_warm_start_ties_on_lattice(ctx):
+    """Warm starts at a non-minimal-index equidistant target must still
+    return the smallest index (the grid path re-ranks every point within the
+    bound, ties included)."""
+    g = np.arange(6, dtype=np.float64)
+    pts = np.array(np.meshgrid(g, g, g, indexing="ij")).reshape(3, -1).T.copy()
+    rng = np.random.default_rng(6)
+    pts = pts[rng.permutation(len(pts))]
+    q = np.array(np.meshgrid(g[:-1] + 0.5, g[:-1] + 0.5, g[:-1] + 0.5, indexing="ij")).reshape(3, -1).T.copy()
+    ctx.set_target(pts)
+    io, do = O.nearest(pts, q)
+    # seed each query with its LARGEST-index equidistant target
+    d2 = ((pts[None, :, :] - q[:, None, :]) ** 2).sum(-1)
+    prev = np.array([np.nonzero(row == row.min())[0].max() for row in d2], np.int32)
+    ig, dg = ctx.nearest(q, prev=prev)
+    assert np.array_equal(ig, io)
+    assert np.array_equal(dg, do)
+
+
+def test_nn_warm_start_surface_with_holes_and_outliers(ctx):
+    """Headline-like geometry: warm start from the previous correspondence of
+    a slightly moved source (the per-pass situation)."""
+    p = R.make_problem(2, scale=0.25)
+    ctx.set_target(p.target)
+    i0, _ = ctx.nearest(p.source)
+    moved = p.source + 0.003 * np.random.default_rng(3).standard_normal(p.source.shape)
+    ig, dg = ctx.nearest(moved, prev=i0)
+    io, do = O.nearest(p.target, moved)
+    _nn_match(ig, dg, io, do)
+
+
 # ------------------------------------------------------------------ components
 @pytest.fixture(scope="module")
 def strip(ctx):
