@@ -222,6 +222,14 @@ struct nrr_ctx {
     bool last_solve_fresh = false;
     int base_iters = 0;
     cudaEvent_t eval_done = nullptr;
+    cudaEvent_t end_done = nullptr;
+    // the next pass's evaluation (terms, energies, device decision) is queued
+    // before the end-of-pass sync, so the GPU works through the host's
+    // end-of-pass processing; invalidated when the stage ends
+    bool eval_queued = false, eval_nn_ran = false, nn_time_pending = false;
+    bool flush_each_pass = false;                 // run_iterate(flush_l2): flush L2 before each queued evaluation
+    std::vector<cudaEvent_t> flush_ev;            // pairs around the in-pass flushes (subtracted from the pass time)
+    int flush_used = 0;
     DevBuf<long long> d_pair_off;
     DevBuf<unsigned char> d_setup_scratch;
     DevBuf<int> d_infl_off, d_infl_node, d_pairs, d_pair_rev, d_node_pair_off, d_row_ptr, d_col, d_ub_cptr, d_cv,
@@ -241,7 +249,7 @@ struct nrr_ctx {
     DevBuf<long long> prof, cta_prof;
     DevBuf<PcgStatus> d_status;
     DevBuf<PassRecord> d_rec;
-    Pinned<PassRecord> h_rec;
+    Pinned<PassRecord> h_rec, h_rec_end;
     Pinned<PcgStatus> h_status;
     Pinned<int> h_deg;
     // Anderson
@@ -278,6 +286,8 @@ struct nrr_ctx {
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
         if (eval_done) cudaEventDestroy(eval_done);
+        if (end_done) cudaEventDestroy(end_done);
+        for (auto& x : flush_ev) cudaEventDestroy(x);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -1025,6 +1035,7 @@ void run_begin(nrr_ctx* c, const nrr_solver_config& cfg_in) {
     RunState& r = c->run;
     r = RunState{};
     c->nn_ready = false;
+    c->eval_queued = false;
     r.t0 = std::chrono::steady_clock::now();
     r.cfg = cfg_in;
     r.lm_idx.assign(cfg_in.landmark_index, cfg_in.landmark_index + cfg_in.landmark_count);
@@ -1078,6 +1089,48 @@ void close_stage(nrr_ctx* c) {
     update_term_weights(r.prm, n_total(c), c->E, c->N, r.cfg);
 }
 
+// Evaluation of a pass at (x, vhat): correspondences (unless queued), terms,
+// energies, the device-side safeguard decision (solver.hpp:239) and the
+// record for the host; eval_done marks its end.
+void queue_eval(nrr_ctx* c, const TermParams& tp, const double* x, const double* vhat) {
+    RunState& r = c->run;
+    NRR_CUDA_CHECK(cudaMemsetAsync(c->d_rec.p, 0, sizeof(PassRecord), c->stream));
+    // warm start from the previous pass's correspondences (init NN at the first pass)
+    c->eval_nn_ran = !c->nn_ready;
+    evaluate(c, x, vhat, tp, true);
+    reduce_energies(c);
+    // the safeguard decision is also taken on the device, so the assembly and
+    // the solve are queued right behind the evaluation and the host's
+    // decision latency hides behind them; on a revert they return at once
+    launch_pass_decision(c->d_rec.p, r.e_prev, r.current_is_aa ? 1 : 0, r.lm_w, c->d_skip.p, c->stream);
+    ++c->launches;
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_deg.p, c->deg.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (c->opt.record_passes == 2) {
+        c->pass_nn.resize(c->pass_nn.size() + c->n);
+        NRR_CUDA_CHECK(cudaMemcpyAsync(c->pass_nn.data() + c->pass_nn.size() - c->n, c->nn_idx.p,
+                                       sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    }
+    NRR_CUDA_CHECK(cudaEventRecord(c->eval_done, c->stream));
+    c->eval_queued = true;
+}
+
+// L2 flush between passes when the caller times with flushed caches: queued
+// right before the next evaluation and timed with its own events, which
+// run_iterate subtracts
+void in_pass_flush(nrr_ctx* c) {
+    if (!c->flush_each_pass) return;
+    while (static_cast<int>(c->flush_ev.size()) < 2 * (c->flush_used + 1)) {
+        cudaEvent_t e;
+        NRR_CUDA_CHECK(cudaEventCreate(&e));
+        c->flush_ev.push_back(e);
+    }
+    NRR_CUDA_CHECK(cudaEventRecord(c->flush_ev[2 * c->flush_used], c->stream));
+    NRR_CUDA_CHECK(cudaMemsetAsync(c->flush.p, c->flush_used & 0xff, c->flush.n * sizeof(double), c->stream));
+    NRR_CUDA_CHECK(cudaEventRecord(c->flush_ev[2 * c->flush_used + 1], c->stream));
+    ++c->flush_used;
+}
+
 // One evaluated pass (solver.hpp:225-288). Returns true when an iteration was
 // accepted; sets *stage_end when the stage converged or hit i_max.
 bool one_pass(nrr_ctx* c, bool* stage_end) {
@@ -1088,26 +1141,11 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     const TermParams tp = local_terms(c, TermParams{r.prm.alpha, r.prm.beta, r.prm.nu_a, r.prm.nu_r, r.lm_w});
     bool ran[nrr_ctx::kClasses];
     std::fill(ran, ran + nrr_ctx::kClasses, false);
-    NRR_CUDA_CHECK(cudaMemsetAsync(c->d_rec.p, 0, sizeof(PassRecord), c->stream));
-    // warm start from the previous pass's correspondences (init NN at the first pass)
-    const bool nn_queued = c->nn_ready;
-    evaluate(c, c->x.p, c->vhat.p, tp, true);
-    reduce_energies(c);
-    ran[kNN] = !nn_queued;  // a queued NN was timed with the previous pass
+    if (!c->eval_queued) queue_eval(c, tp, c->x.p, c->vhat.p);
+    c->eval_queued = false;
+    ran[kNN] = c->eval_nn_ran || c->nn_time_pending;  // a queued NN is harvested with its evaluation
+    c->nn_time_pending = false;
     ran[kTerms] = true;
-    // the safeguard decision is also taken on the device, so the assembly and
-    // the solve are queued right behind the evaluation and the host's
-    // decision latency hides behind them; on a revert they return at once
-    launch_pass_decision(c->d_rec.p, r.e_prev, r.current_is_aa ? 1 : 0, r.lm_w, c->d_skip.p, c->stream);
-    ++c->launches;
-    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
-    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_deg.p, c->deg.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    if (c->opt.record_passes == 2) {
-        c->pass_nn.resize(c->pass_nn.size() + n);
-        NRR_CUDA_CHECK(cudaMemcpyAsync(c->pass_nn.data() + c->pass_nn.size() - n, c->nn_idx.p, sizeof(int) * n,
-                                       cudaMemcpyDeviceToHost, c->stream));
-    }
-    NRR_CUDA_CHECK(cudaEventRecord(c->eval_done, c->stream));
     c->dp.skip = c->d_skip.p;
     assemble(c, tp);
     if (c->comm) {  // the replicated solve needs the full K and B (north_star: allreduce before the solve)
@@ -1134,6 +1172,8 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
         deform_run(c, c->x.p, c->vhat.p, nullptr, nullptr);
         r.current_is_aa = false;
         ++r.st.reverts;
+        in_pass_flush(c);
+        queue_eval(c, tp, c->x.p, c->vhat.p);  // the next pass re-evaluates at x_mm
         return false;
     }
     r.e_prev = e_accept;
@@ -1148,15 +1188,18 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     ran[kDeform] = true;
     allreduce(c, &c->d_rec.p->max_disp, 1, ncclFloat64, ncclMax);
     allreduce(c, &c->d_rec.p->nonfinite, 1, ncclInt32, ncclMax);
-    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_rec_end.p, c->d_rec.p, sizeof(PassRecord), cudaMemcpyDeviceToHost, c->stream));
     NRR_CUDA_CHECK(cudaMemcpyAsync(c->h_status.p, c->d_status.p, sizeof(PcgStatus), cudaMemcpyDeviceToHost, c->stream));
-    // the next pass's correspondences at the new iterate (independent of the
-    // host's end-of-pass decisions; a new stage only changes the weights) are
-    // queued before the sync, so the GPU does not idle through it
+    NRR_CUDA_CHECK(cudaEventRecord(c->end_done, c->stream));
+    // the next pass's correspondences and evaluation at the new iterate are
+    // queued before the end-of-pass sync (a new stage only changes the
+    // weights: then the queued evaluation is dropped and redone)
+    in_pass_flush(c);
     nn_run(c, c->vhat2.p, c->n, c->nn_idx.p, c->nn_idx.p, c->d2.p, c->q.p, c->d_anchor.p);
     c->nn_ready = true;
-    ran[kNN] = true;
-    sync(c);
+    c->nn_time_pending = true;
+    queue_eval(c, tp, c->xnext.p, c->vhat2.p);
+    NRR_CUDA_CHECK(cudaEventSynchronize(c->end_done));
     harvest(c, ran);
     check_pcg(c, *c->h_status.p);
     c->pcg_iters_total += c->h_status.p->iterations;
@@ -1165,8 +1208,8 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
         if (c->last_solve_fresh) c->base_iters = it;
         else if (it > c->base_iters + c->base_iters / 4 + 2) c->sub_age = c->coarse_age = -1;
     }
-    if (c->h_rec.p->nonfinite) throw NumericalError("solver aborted: iterate is not finite");
-    rec.max_disp = c->h_rec.p->max_disp;
+    if (c->h_rec_end.p->nonfinite) throw NumericalError("solver aborted: iterate is not finite");
+    rec.max_disp = c->h_rec_end.p->max_disp;
     c->iters.push_back(rec);
     ++r.st.iteration_count;
     std::swap(c->x.p, c->xnext.p);
@@ -1177,6 +1220,10 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
         *stage_end = true;
     } else if (r.accepted >= r.cfg.i_max) {
         *stage_end = true;
+    }
+    if (*stage_end) {  // the queued evaluation used this stage's weights
+        c->eval_queued = false;
+        c->nn_ready = true;  // the correspondences at x stay valid
     }
     return true;
 }
@@ -1189,26 +1236,40 @@ int run_iterate(nrr_ctx* c, int max_accepted, bool flush_l2, double* device_ms) 
     if (!r.active) throw ConfigError("no registration in progress (nrr_ctx_begin)");
     int acc = 0;
     if (flush_l2 && c->flush.n == 0) c->flush.resize(c->l2_bytes * 2 / sizeof(double) + 1);
+    c->flush_each_pass = flush_l2;
+    c->flush_used = 0;
+    // one event interval around all the passes of this call (host gaps
+    // included), minus the flushes queued inside it; a flush before the first
+    // evaluation (when none is queued) stays outside the interval
+    if (flush_l2 && !c->eval_queued)
+        NRR_CUDA_CHECK(cudaMemsetAsync(c->flush.p, 0x5a, c->flush.n * sizeof(double), c->stream));
+    NRR_CUDA_CHECK(cudaEventRecord(c->pass_ev[0], c->stream));
     while (!r.done && acc < max_accepted) {
         if (!r.stage_open) open_stage(c);
-        if (flush_l2) NRR_CUDA_CHECK(cudaMemsetAsync(c->flush.p, acc & 0xff, c->flush.n * sizeof(double), c->stream));
-        NRR_CUDA_CHECK(cudaEventRecord(c->pass_ev[0], c->stream));
         bool stage_end = false;
         const bool accepted = one_pass(c, &stage_end);
-        NRR_CUDA_CHECK(cudaEventRecord(c->pass_ev[1], c->stream));
-        NRR_CUDA_CHECK(cudaEventSynchronize(c->pass_ev[1]));
-        float ms = 0.f;
-        NRR_CUDA_CHECK(cudaEventElapsedTime(&ms, c->pass_ev[0], c->pass_ev[1]));
-        if (device_ms) *device_ms += ms;
         if (accepted) ++acc;
         if (stage_end) close_stage(c);
     }
+    NRR_CUDA_CHECK(cudaEventRecord(c->pass_ev[1], c->stream));
+    NRR_CUDA_CHECK(cudaEventSynchronize(c->pass_ev[1]));
+    float ms = 0.f;
+    NRR_CUDA_CHECK(cudaEventElapsedTime(&ms, c->pass_ev[0], c->pass_ev[1]));
+    double total = ms;
+    for (int k = 0; k < c->flush_used; ++k) {
+        float f = 0.f;
+        NRR_CUDA_CHECK(cudaEventElapsedTime(&f, c->flush_ev[2 * k], c->flush_ev[2 * k + 1]));
+        total -= f;
+    }
+    c->flush_each_pass = false;
+    if (device_ms) *device_ms += total;
     return acc;
 }
 
 void run_finish(nrr_ctx* c, double* out_X, double* out_deformed) {
     RunState& r = c->run;
     c->nn_ready = false;
+    c->eval_queued = false;
     if (!r.active) throw ConfigError("no registration in progress (nrr_ctx_begin)");
     if (r.stage_open) close_stage(c);  // stopped early: record the partial stage
     const auto t2 = std::chrono::steady_clock::now();
@@ -1280,6 +1341,7 @@ int nrr_ctx_create(int device, nrr_ctx** out) {
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->eval_done, cudaEventDisableTiming));
+        NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->end_done, cudaEventDisableTiming));
         c->d_rec.resize(1);
         c->d_status.resize(1);
         c->deg.resize(1);
