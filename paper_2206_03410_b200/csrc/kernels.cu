@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_kernel(DevProblem p, 
     for (int i = 0; i < 32; ++i) v[i] = 0.0;
     for (int t = cb + lane; t < ce; t += 32) {
         const int vtx = p.c_v[t];
-        const double4 fa = p.infl_f[p.c_ea[t]];
+        const double4 fa = p.c_fa[t];
         const double w = wa[vtx];
         const double a4[4] = {fa.x, fa.y, fa.z, fa.w};
         if (diag) {
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_kernel(DevProblem p, 
                 for (int c = 0; c < 3; ++c) v[16 + 3 * r + c] += wr_ * q3[c];
             }
         } else {
-            const double4 fb = p.infl_f[p.c_eb[t]];
+            const double4 fb = p.c_fb[t];
             const double b4[4] = {fb.x, fb.y, fb.z, fb.w};
 #pragma unroll
             for (int r = 0; r < 4; ++r)

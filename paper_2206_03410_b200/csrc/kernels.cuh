@@ -35,6 +35,8 @@ struct DevProblem {
     const int* c_v = nullptr;          // contributor vertex
     const int* c_ea = nullptr;         // contributor influence entry of the row node
     const int* c_eb = nullptr;         // contributor influence entry of the column node
+    const double4* c_fa = nullptr;     // infl_f[c_ea] per contributor (streamed, not gathered)
+    const double4* c_fb = nullptr;     // infl_f[c_eb] per contributor
     const int* ub_kpos = nullptr;      // BSR block (a, b)
     const int* ub_kpos_t = nullptr;    // BSR block (b, a)
     const int* edges = nullptr;        // E*2

@@ -205,7 +205,7 @@ struct nrr_ctx {
     std::vector<double> h_src;
     DevBuf<double> d_src, d_infl_w, d_anchor, d_node_pos, d_pair_c;
     std::vector<double> h_anchor;  // sum_a w_a p_a per vertex (energy.hpp:150-161)
-    DevBuf<double4> d_infl_f, d_pair_gv;
+    DevBuf<double4> d_infl_f, d_pair_gv, d_cfa, d_cfb;
     DevBuf<double> d_med_sorted;
     DevBuf<unsigned long long> nn_stats;
     DevBuf<unsigned char> d_med_tmp;
@@ -561,6 +561,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->d_pair_off.upload(pair_off.data(), pair_off.size(), s);
         c->d_ub_cptr.resize(U + 1);
         for (auto* b : {&c->d_cv, &c->d_cea, &c->d_ceb}) b->resize(std::max<long long>(entries, 1));
+        for (auto* b : {&c->d_cfa, &c->d_cfb}) b->resize(std::max<long long>(entries, 1));
         c->d_setup_flags.resize(1);
         c->d_setup_scratch.resize(setup_gpu_scratch_bytes(entries, U));
         SetupGpuIn in;
@@ -584,6 +585,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         out.cv = c->d_cv.p;
         out.cea = c->d_cea.p;
         out.ceb = c->d_ceb.p;
+        out.cfa = c->d_cfa.p;
+        out.cfb = c->d_cfb.p;
         out.flags = c->d_setup_flags.p;
         build_setup_gpu(in, entries, out, c->d_setup_scratch.p, s);
         c->launches += 4;
@@ -619,6 +622,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     d.c_v = c->d_cv.p;
     d.c_ea = c->d_cea.p;
     d.c_eb = c->d_ceb.p;
+    d.c_fa = c->d_cfa.p;
+    d.c_fb = c->d_cfb.p;
     d.ub_kpos = c->d_ub_kpos.p;
     d.ub_kpos_t = c->d_ub_kpos_t.p;
     d.edges = c->d_edges.p;

@@ -93,13 +93,17 @@ __global__ void emit_kernel(SetupGpuIn in, int* __restrict__ key, int* __restric
 
 __global__ void gather_kernel(long long count, const int* __restrict__ order, const int* __restrict__ ei,
                               const int* __restrict__ ea, const int* __restrict__ eb, int* __restrict__ cv,
-                              int* __restrict__ cea, int* __restrict__ ceb) {
+                              int* __restrict__ cea, int* __restrict__ ceb, const double4* __restrict__ f,
+                              double4* __restrict__ cfa, double4* __restrict__ cfb) {
     const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (p >= count) return;
     const int q = order[p];
+    const int a = ea[q], b = eb[q];
     cv[p] = ei[q];
-    cea[p] = ea[q];
-    ceb[p] = eb[q];
+    cea[p] = a;
+    ceb[p] = b;
+    cfa[p] = f[a];
+    cfb[p] = f[b];
 }
 
 int key_bits(int U) {
@@ -177,7 +181,8 @@ void build_setup_gpu(const SetupGpuIn& in, long long entries, const SetupGpuOut&
     tb = sc.cub_bytes;
     NRR_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(sc.cub_tmp, tb, sc.ucnt, out.cptr, in.U + 1, s));
     const int gb = static_cast<int>((entries + kSetupThreads - 1) / kSetupThreads);
-    gather_kernel<<<gb, kSetupThreads, 0, s>>>(entries, sc.val_out, sc.ei, sc.ea, sc.eb, out.cv, out.cea, out.ceb);
+    gather_kernel<<<gb, kSetupThreads, 0, s>>>(entries, sc.val_out, sc.ei, sc.ea, sc.eb, out.cv, out.cea, out.ceb,
+                                               out.infl_f, out.cfa, out.cfb);
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 

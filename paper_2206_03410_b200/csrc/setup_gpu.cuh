@@ -31,6 +31,8 @@ struct SetupGpuOut {
     int* cv = nullptr;          // entries: vertex
     int* cea = nullptr;         // entries: influence index a
     int* ceb = nullptr;         // entries: influence index b
+    double4* cfa = nullptr;     // entries: infl_f[a] (materialised: the assembly streams it instead of gathering)
+    double4* cfb = nullptr;     // entries: infl_f[b]
     int* flags = nullptr;       // 1 int: bit 0 = a co-influencing pair is not a graph edge
 };
 
