@@ -220,6 +220,8 @@ __device__ void block_gj_inverse(double* A, int nm, const int* blocks, int ld, s
 // psi_k(a)^T K_ab psi_l(b). One thread per block forms its 4x4 projection
 // (staged in shared memory), then 8 lanes per output sum the blocks of that
 // aggregate (lane-strided, butterfly-combined): deterministic, no atomics.
+constexpr int kCpChunk = 1024;  // blocks per shared-memory pass (a multiple of 8: same sum order as one pass)
+constexpr int kCpRounds = 16;   // 64 touched aggregates x 16 entries / 64 lane groups
 __global__ void __launch_bounds__(kCoarseThreads) coarse_partial_kernel(PcgArgs a, double* __restrict__ partial) {
     if (a.skip != nullptr && *a.skip) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -227,54 +229,71 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_partial_kernel(PcgArgs 
     const int r0 = a.row_begin[c], r1 = a.row_begin[c + 1];
     const int kb0 = a.row_ptr[r0], nkb = a.row_ptr[r1] - kb0;
     const int t0 = a.touch_off[c], nt = a.touch_off[c + 1] - t0;
-    double* Pb = reinterpret_cast<double*>(smem_raw);                 // nkb*16
-    int* tb = reinterpret_cast<int*>(Pb + 16 * static_cast<size_t>(nkb));  // nkb: touched index of the column aggregate
-    int* rowof = tb + nkb;                                            // nkb: local row of the block
+    const int chunk = min(kCpChunk, (a.max_kb + 7) & ~7);                   // shared-memory capacity in blocks
+    double* Pb = reinterpret_cast<double*>(smem_raw);                         // chunk*16
+    int* tb = reinterpret_cast<int*>(Pb + 16 * static_cast<size_t>(chunk));  // touched index of the column aggregate
+    int* rowof = tb + chunk;                                                  // solver row of the block
     __shared__ int s_touch[64];
     for (int t = threadIdx.x; t < nt && t < 64; t += blockDim.x) s_touch[t] = a.touch_agg[t0 + t];
-    for (int j = r0 + threadIdx.x; j < r1; j += blockDim.x)
-        for (int b = a.row_ptr[j]; b < a.row_ptr[j + 1]; ++b) rowof[b - kb0] = j;
-    __syncthreads();
-    for (int lb = threadIdx.x; lb < nkb; lb += blockDim.x) {
-        const int na = a.row_node[rowof[lb]], nb = a.col[kb0 + lb];
-        double d[3], e[3];
-        node_offset(a, na, d);
-        node_offset(a, nb, e);
-        const int hb = a.node_agg[nb];
-        int t = 0;
-        while (t < nt - 1 && s_touch[t] != hb) ++t;
-        tb[lb] = t;
-        const double* K = a.K + static_cast<size_t>(kb0 + lb) * 16;
-        double k4[16];
+    const int l8 = threadIdx.x & 7, g8 = threadIdx.x >> 3, ngroups = blockDim.x >> 3;
+    double acc[kCpRounds];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) k4[q] = K[q];
-        double u[4][4];  // u = K_ab psi(b)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-#pragma unroll
-            for (int l = 0; l < 3; ++l) u[r][l] = k4[r * 4 + l] + e[l] * k4[r * 4 + 3];
-            u[r][3] = k4[r * 4 + 3];
+    for (int q = 0; q < kCpRounds; ++q) acc[q] = 0.0;
+    for (int cb = 0; cb < nkb; cb += chunk) {  // large subdomains: several passes
+        const int ce = min(nkb, cb + chunk);
+        __syncthreads();  // the previous chunk's reads are done
+        for (int j = r0 + threadIdx.x; j < r1; j += blockDim.x) {
+            const int b0 = max(a.row_ptr[j] - kb0, cb), b1 = min(a.row_ptr[j + 1] - kb0, ce);
+            for (int b = b0; b < b1; ++b) rowof[b - cb] = j;
         }
+        __syncthreads();
+        for (int lb = cb + threadIdx.x; lb < ce; lb += blockDim.x) {
+            const int x = lb - cb;
+            const int na = a.row_node[rowof[x]], nb = a.col[kb0 + lb];
+            double d[3], e[3];
+            node_offset(a, na, d);
+            node_offset(a, nb, e);
+            const int hb = a.node_agg[nb];
+            int t = 0;
+            while (t < nt - 1 && s_touch[t] != hb) ++t;
+            tb[x] = t;
+            const double* K = a.K + static_cast<size_t>(kb0 + lb) * 16;
+            double k4[16];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
+            for (int q = 0; q < 16; ++q) k4[q] = K[q];
+            double u[4][4];  // u = K_ab psi(b)
 #pragma unroll
-            for (int k = 0; k < 3; ++k) Pb[lb * 16 + k * 4 + l] = u[k][l] + d[k] * u[3][l];
-            Pb[lb * 16 + 12 + l] = u[3][l];
+            for (int r = 0; r < 4; ++r) {
+#pragma unroll
+                for (int l = 0; l < 3; ++l) u[r][l] = k4[r * 4 + l] + e[l] * k4[r * 4 + 3];
+                u[r][3] = k4[r * 4 + 3];
+            }
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) Pb[x * 16 + k * 4 + l] = u[k][l] + d[k] * u[3][l];
+                Pb[x * 16 + 12 + l] = u[3][l];
+            }
+        }
+        __syncthreads();
+        // 8 lanes per output entry, lane-strided over the blocks (ascending lb)
+#pragma unroll
+        for (int q = 0; q < kCpRounds; ++q) {
+            const int o = q * ngroups + g8;
+            if (o >= nt * 16) continue;
+            const int t = o >> 4, kl = o & 15;
+            for (int x = l8; x < ce - cb; x += 8)
+                if (tb[x] == t) acc[q] += Pb[x * 16 + kl];
         }
     }
-    __syncthreads();
-    const int l8 = threadIdx.x & 7;
-    for (int o0 = 0; o0 < nt * 16; o0 += blockDim.x >> 3) {  // uniform trip count: full-warp shuffles
-        const int o = o0 + (threadIdx.x >> 3);
-        double s = 0.0;
-        if (o < nt * 16) {
-            const int t = o >> 4, kl = o & 15;
-            for (int lb = l8; lb < nkb; lb += 8)
-                if (tb[lb] == t) s += Pb[lb * 16 + kl];
-        }
 #pragma unroll
-        for (int off = 4; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (l8 == 0 && o < nt * 16) partial[(static_cast<size_t>(c) * a.max_touch + (o >> 4)) * 16 + (o & 15)] = s;
+    for (int q = 0; q < kCpRounds; ++q) {
+        if (q * ngroups >= nt * 16) break;  // uniform: full-warp shuffles
+        double v = acc[q];
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        const int o = q * ngroups + g8;
+        if (l8 == 0 && o < nt * 16) partial[(static_cast<size_t>(c) * a.max_touch + (o >> 4)) * 16 + (o & 15)] = v;
     }
 }
 
@@ -1556,13 +1575,15 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
                          3 * kCoarseMax /* ptq */ + 12 * static_cast<size_t>(max_ext) /* ext */ +
                          (max_rows + 1) / 2 /* rchunk */ + (max_ext + 1) / 2 /* tl */ + 2;
     const size_t kbytes = static_cast<size_t>(max_kb) * (16 * sizeof(double) + sizeof(int));
-    k_in_smem = sizeof(double) * fixed + kbytes + 64 <= smem_limit;
     // largest subdomain chunk (rows per dense block-Jacobi inverse) that fits
     auto sub_doubles = [&](int S) {
         const int ld = sub_leading_dim(S);
         const size_t ch = (max_rows + S - 1) / S;
         return ch * 4 * static_cast<size_t>(S) * ld + (ch + 2) / 2;
     };
+    // K stays in shared memory when it fits beside the smallest (1-node)
+    // subdomain plan; otherwise the SpMV reads it from L2
+    k_in_smem = sizeof(double) * (fixed + sub_doubles(1)) + kbytes + 64 <= smem_limit;
     int S = std::max(1, std::min(max_rows, kSubRowsMax));  // largest chunk that fits; NRR_SUB_ROWS overrides
     if (const char* e = std::getenv("NRR_SUB_ROWS")) S = std::max(1, std::min(max_rows, std::atoi(e)));
     const size_t kpart = k_in_smem ? kbytes : 0;
@@ -1574,14 +1595,19 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
     sub_ld = sub_leading_dim(S);
     sub_chunks = (max_rows + S - 1) / S;
     smem_bytes = sizeof(double) * (fixed + sub_doubles(S)) + kpart + 64;
-    if (smem_bytes > smem_limit) throw ConfigError("PCG: shared-memory plan does not fit");
+    if (smem_bytes > smem_limit)
+        throw ConfigError("PCG: shared-memory plan does not fit (" + std::to_string(smem_bytes) + " > " +
+                          std::to_string(smem_limit) + " bytes; fixed " + std::to_string(fixed * sizeof(double)) +
+                          ", max_rows " + std::to_string(max_rows) + ", max_ext " + std::to_string(max_ext) + ")");
 }
 
 void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s) {
-    const size_t psmem = static_cast<size_t>(plan.max_kb) * (16 * sizeof(double) + 2 * sizeof(int)) + 64;
+    const size_t psmem =
+        static_cast<size_t>(std::min((plan.max_kb + 7) & ~7, kCpChunk)) * (16 * sizeof(double) + 2 * sizeof(int)) + 64;
     allow_max_smem(reinterpret_cast<const void*>(coarse_partial_kernel));
     PcgArgs b = a;
     b.max_touch = plan.max_touch;
+    b.max_kb = plan.max_kb;
     coarse_partial_kernel<<<plan.grid, kCoarseThreads, psmem, s>>>(b, w.partial);
     NRR_CUDA_CHECK(cudaGetLastError());
     const int nc = 4 * plan.n_agg;

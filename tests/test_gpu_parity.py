@@ -407,3 +407,30 @@ def test_repeat_runs_bitwise_identical():
     a = _fixed_count_run(p, 15)
     b = _fixed_count_run(p, 15)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+
+
+@pytest.mark.parametrize("cap", [3, 6])
+def test_step_parity_large_subdomains(cap):
+    """The PCG paths the headline config does not take: a grid capped at a few
+    CTAs gives hundreds of nodes per CTA, i.e. several elements per thread
+    (EPT 4/8), K read from L2 instead of shared memory, small subdomain
+    chunks and a coarse space of one or two aggregates. Same teacher-forced
+    pass as test_step_parity: the solve must meet the reference bar."""
+    p = R.make_problem(1, scale=0.4)
+    c = R.Context(max_ctas=cap)
+    try:
+        c.set_problem(p)
+        c.set_target(p.target)
+        N = p.graph.node_count
+        row_ptr, _ = R.bsr_pattern(p.graph)
+        nnzb = int(row_ptr[-1])
+        X = random_transforms(N, 7, 0.1)
+        prm = (0.8, 1.7, 0.09, 0.12)
+        g = c.step(X, prm, nnzb=nnzb)
+        o = O.step(p, X, prm, nnzb)
+        assert np.array_equal(g["index"], o["index"])
+        assert np.allclose(g["energy"], o["energy"], rtol=1e-12, atol=0)
+        err = np.max(np.abs(g["Xmm"] - o["Xmm"]))
+        assert err <= 1e-8 * (1 + np.max(np.abs(o["Xmm"]))), err
+    finally:
+        c.close()
