@@ -409,7 +409,7 @@ def test_repeat_runs_bitwise_identical():
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
 
 
-@pytest.mark.parametrize("cap", [3, 6])
+@pytest.mark.parametrize("cap", [3, 6, 12])
 def test_step_parity_large_subdomains(cap):
     """The PCG paths the headline config does not take: a grid capped at a few
     CTAs gives hundreds of nodes per CTA, i.e. several elements per thread
