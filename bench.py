@@ -183,6 +183,20 @@ def iteration_fixed_bytes(n, m, sumk, N, P, mk=5):
     return per_vertex + target + node + aa
 
 
+def kernel_bytes(n, m, sumk, N, P, entries, mk=5):
+    """Algorithmic bytes per MM pass of each kernel class (DESIGN.md section 3;
+    SURVEY.md 8(d) split by kernel): compulsory HBM reads + writes, gathers of
+    L2-resident node data not counted."""
+    kbar = sumk / n
+    return {
+        "deform": (24 + 4 + 12 * kbar + 24 + 24) * n,           # src, influence CSR, old v, new v
+        "nn": 24 * n + 16 * m + 4 * n + 8 * n + 24 * n,         # queries, target, prev idx, out idx/d2/q
+        "terms": (8 + 8) * n + 16 * P + 8 * P + 4 * 96 * N,     # d2 -> w_a, pairs -> w_r, X/R
+        "assemble": 128 * (N + P) + 96 * N + entries * (4 + 64) + n * (8 + 24),  # K, B, contributors, w_a, q
+        "aa": (2 * mk + 4) * 96 * N,
+    }
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -269,6 +283,8 @@ def run_b200(args, dist):
         p = p_full
     g = p.graph
     n, m, N, P, sumk = p.n, len(p.target), g.node_count, g.pair_count, len(g.infl_nodes)
+    kk = np.diff(np.asarray(g.infl_offsets, dtype=np.int64))
+    entries = int(np.sum(kk * (kk + 1) // 2))  # assembly contributor entries
     ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
     if sharded:
         join_shard(R, ctx, dist, p_full.n)
@@ -354,6 +370,9 @@ def run_b200(args, dist):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms},
             "step_roofline": {"achieved": step_gbs, "frac": step_gbs / peak, "bytes_per_step": step_bytes},
+            "kernel_roofline": {k: {"bytes": b, "achieved_gbs": b / (kms[k] / K / 1e3) / 1e9,
+                                    "frac": b / (kms[k] / K / 1e3) / 1e9 / peak}
+                                for k, b in kernel_bytes(n, m, sumk, N, P, entries).items() if kms.get(k, 0) > 0},
             "kernel_ms_per_step": {k: v / K for k, v in kms.items()},
             "pcg_iterations_per_step": pcg_iters / K,
             "nn_queries_per_s": n / (kms["nn"] / K / 1e3) if kms["nn"] > 0 else None,

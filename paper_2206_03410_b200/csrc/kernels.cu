@@ -53,11 +53,22 @@ __global__ void __launch_bounds__(256) deform_kernel(DevProblem p, const double*
             disp = sqrt(ex * ex + ey * ey + ez * ez);
         }
     }
+    // one global atomic per block (max is exact in any order): a per-warp
+    // atomic on one address serialised ~31K updates at 1M vertices
+    __shared__ double s_max[8];
     if (max_disp) {
         disp = warp_max(disp);
-        if ((threadIdx.x & 31) == 0 && disp > 0.0) atomic_max_nonneg(max_disp, disp);
+        if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = disp;
     }
-    if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+    const int any_bad = __syncthreads_or(bad ? 1 : 0);
+    if (threadIdx.x == 0) {
+        if (max_disp) {
+            double m = s_max[0];
+            for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, s_max[w]);
+            if (m > 0.0) atomic_max_nonneg(max_disp, m);
+        }
+        if (nonfinite && any_bad) atomicOr(nonfinite, 1);
+    }
 }
 
 // ---------------------------------------------------------------- terms
