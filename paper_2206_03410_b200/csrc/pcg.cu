@@ -1052,36 +1052,57 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     };
     auto spmv = [&](int k) -> double {
         const int b0 = el_b0[k], b1 = el_b1[k];  // empty range for dead elements
-        // two independent chains (even / odd blocks) halve the FMA latency chain
-        double acc0 = 0.0, acc1 = 0.0;
+        // four independent chains, all of a group's loads issued before its
+        // FMAs (K comes from L2 when it does not fit in shared memory)
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
         int b = b0;
-        for (; b + 1 < b1; b += 2) {
-            const int c0 = sh.col[b], c1 = sh.col[b + 1];
-            const double* k0 = sh.K + static_cast<size_t>(b) * 16 + my_r * 4;
-            const double2 ka0 = *reinterpret_cast<const double2*>(k0);
-            const double2 ka1 = *reinterpret_cast<const double2*>(k0 + 2);
-            const double2 kb0 = *reinterpret_cast<const double2*>(k0 + 16);
-            const double2 kb1 = *reinterpret_cast<const double2*>(k0 + 18);
-            const double* v0 = sh.ext + c0 * 12 + my_c;
-            const double* v1 = sh.ext + c1 * 12 + my_c;
-            acc0 = fma(ka0.x, v0[0], acc0);
-            acc1 = fma(kb0.x, v1[0], acc1);
-            acc0 = fma(ka0.y, v0[3], acc0);
-            acc1 = fma(kb0.y, v1[3], acc1);
-            acc0 = fma(ka1.x, v0[6], acc0);
-            acc1 = fma(kb1.x, v1[6], acc1);
-            acc0 = fma(ka1.y, v0[9], acc0);
-            acc1 = fma(kb1.y, v1[9], acc1);
+        for (; b + 3 < b1; b += 4) {
+            int cc[4];
+            double2 ka[4], kb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                cc[u] = sh.col[b + u];
+                const double* kp = sh.K + static_cast<size_t>(b + u) * 16 + my_r * 4;
+                ka[u] = *reinterpret_cast<const double2*>(kp);
+                kb[u] = *reinterpret_cast<const double2*>(kp + 2);
+            }
+            double vv[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double* v = sh.ext + cc[u] * 12 + my_c;
+                vv[u][0] = v[0];
+                vv[u][1] = v[3];
+                vv[u][2] = v[6];
+                vv[u][3] = v[9];
+            }
+            acc0 = fma(ka[0].x, vv[0][0], acc0);
+            acc1 = fma(ka[1].x, vv[1][0], acc1);
+            acc2 = fma(ka[2].x, vv[2][0], acc2);
+            acc3 = fma(ka[3].x, vv[3][0], acc3);
+            acc0 = fma(ka[0].y, vv[0][1], acc0);
+            acc1 = fma(ka[1].y, vv[1][1], acc1);
+            acc2 = fma(ka[2].y, vv[2][1], acc2);
+            acc3 = fma(ka[3].y, vv[3][1], acc3);
+            acc0 = fma(kb[0].x, vv[0][2], acc0);
+            acc1 = fma(kb[1].x, vv[1][2], acc1);
+            acc2 = fma(kb[2].x, vv[2][2], acc2);
+            acc3 = fma(kb[3].x, vv[3][2], acc3);
+            acc0 = fma(kb[0].y, vv[0][3], acc0);
+            acc1 = fma(kb[1].y, vv[1][3], acc1);
+            acc2 = fma(kb[2].y, vv[2][3], acc2);
+            acc3 = fma(kb[3].y, vv[3][3], acc3);
         }
-        if (b < b1) {
+        for (; b < b1; ++b) {
             const double* kk = sh.K + static_cast<size_t>(b) * 16 + my_r * 4;
-            const double* vv = sh.ext + sh.col[b] * 12 + my_c;
-            acc0 = fma(kk[0], vv[0], acc0);
-            acc0 = fma(kk[1], vv[3], acc0);
-            acc0 = fma(kk[2], vv[6], acc0);
-            acc0 = fma(kk[3], vv[9], acc0);
+            const double* v = sh.ext + sh.col[b] * 12 + my_c;
+            acc0 = fma(kk[0], v[0], acc0);
+            acc0 = fma(kk[1], v[3], acc0);
+            acc0 = fma(kk[2], v[6], acc0);
+            acc0 = fma(kk[3], v[9], acc0);
         }
-        return acc0 + acc1;
+        acc0 += acc1;
+        acc2 += acc3;
+        return acc0 + acc2;
     };
     // Psi^T contribution of the thread's elements (own column): 4 mode sums
     auto psi_acc = [&](int k, double v, double ps[4]) {
