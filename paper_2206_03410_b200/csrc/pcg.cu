@@ -1209,6 +1209,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             double c0 = 0.0, c1 = 0.0, c2 = 0.0;
             if (row < 4 * nt) {
                 const double* ci = sh.cinv + static_cast<size_t>(row) * nc;
+#pragma unroll 4
                 for (int j = l8; j < nc; j += 8) {
                     const double w = ci[j];
                     c0 = fma(w, sh.ptq[3 * j], c0);
