@@ -506,6 +506,10 @@ def run_pairs(args, dist):
 
 
 def main():
+    if os.environ.get("BENCH_TRACEBACK_AFTER"):  # debugging aid: dump all thread stacks after N seconds
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["BENCH_TRACEBACK_AFTER"]), exit=True)
     args = parse()
     dist = Dist()
     if args.impl == "reference":

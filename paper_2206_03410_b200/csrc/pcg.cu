@@ -34,6 +34,11 @@
 #include <cmath>
 #include <cstdlib>
 #include <numeric>
+#include <vector>
+#include <chrono>
+#include <mutex>
+#include <map>
+#include <condition_variable>
 #include <thread>
 
 #include "device_common.cuh"
@@ -1660,7 +1665,58 @@ void launch_sub_invert(const PcgPlan& plan, const PcgArgs& a, double* out, cudaS
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
+namespace {
+// Cooperative grids in flight per device, each with the event recorded after
+// its launch (polled: no stream callback on the critical path).
+struct CoopBudget {
+    std::mutex mu;
+    std::map<int, std::vector<std::pair<cudaEvent_t, int>>> inflight;
+    void acquire(int dev, int ctas, int sms, cudaEvent_t ev) {
+        std::unique_lock<std::mutex> lk(mu);
+        auto& v = inflight[dev];
+        // the caller's previous grid has completed (the host synchronised
+        // its stream since): its entry goes before the event is reused
+        for (size_t k = 0; k < v.size(); ++k)
+            if (v[k].first == ev) {
+                v.erase(v.begin() + static_cast<long>(k));
+                break;
+            }
+        while (true) {
+            int used = 0;
+            for (size_t k = 0; k < v.size();) {
+                if (cudaEventQuery(v[k].first) != cudaErrorNotReady) {
+                    v.erase(v.begin() + static_cast<long>(k));
+                } else {
+                    used += v[k].second;
+                    ++k;
+                }
+            }
+            if (used == 0 || used + ctas <= sms) break;
+            lk.unlock();
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+            lk.lock();
+        }
+        v.push_back({ev, ctas});
+    }
+    void forget(cudaEvent_t ev) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& [d, v] : inflight)
+            for (size_t k = 0; k < v.size(); ++k)
+                if (v[k].first == ev) {
+                    v.erase(v.begin() + static_cast<long>(k));
+                    break;
+                }
+    }
+};
+CoopBudget& coop_budget() {
+    static CoopBudget b;
+    return b;
+}
+}  // namespace
+
+void pcg_forget_event(cudaEvent_t ev) { coop_budget().forget(ev); }
+
+void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s, cudaEvent_t done) {
     args.max_rows = plan.max_rows;
     args.sub_rows = plan.sub_rows;
     args.sub_ld = plan.sub_ld;
@@ -1693,7 +1749,17 @@ void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s) {
                         std::to_string(fa.sharedSizeBytes) + ", dynamic smem " + std::to_string(plan.smem_bytes) +
                         ", local " + std::to_string(fa.localSizeBytes));
     }
+    // Several contexts may launch their PCG grids side by side (config 3).
+    // A grid spins at its barriers, so two partially resident grids could
+    // wait on each other's SMs; a per-device budget keeps the sum of the
+    // cooperative grids in flight within one CTA per SM. The budget is
+    // returned by a host callback when the kernel has finished.
+    int dev = 0, sms = 0;
+    NRR_CUDA_CHECK(cudaGetDevice(&dev));
+    NRR_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    coop_budget().acquire(dev, plan.grid, sms, done);
     NRR_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kPcgThreads), kargs, plan.smem_bytes, s));
+    NRR_CUDA_CHECK(cudaEventRecord(done, s));
 }
 
 }  // namespace nrr_b200

@@ -94,6 +94,9 @@ struct CoarseWork {
 void launch_coarse_setup(const PcgPlan& plan, const PcgArgs& a, const CoarseWork& w, cudaStream_t s);
 // dense inverses of the subdomain diagonal blocks (one CTA per PCG CTA)
 void launch_sub_invert(const PcgPlan& plan, const PcgArgs& a, double* out, cudaStream_t s);
-void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s);
+// `done` (one per caller, reused): recorded after the launch; cooperative grids
+// in flight on the device are kept within one CTA per SM in total
+void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s, cudaEvent_t done);
+void pcg_forget_event(cudaEvent_t done);
 
 }  // namespace nrr_b200

@@ -223,6 +223,7 @@ struct nrr_ctx {
     int base_iters = 0;
     cudaEvent_t eval_done = nullptr;
     cudaEvent_t end_done = nullptr;
+    cudaEvent_t pcg_done = nullptr;  // after each PCG launch (device budget of cooperative grids)
     // the next pass's evaluation (terms, energies, device decision) is queued
     // before the end-of-pass sync, so the GPU works through the host's
     // end-of-pass processing; invalidated when the stage ends
@@ -287,6 +288,10 @@ struct nrr_ctx {
         if (join) cudaEventDestroy(join);
         if (eval_done) cudaEventDestroy(eval_done);
         if (end_done) cudaEventDestroy(end_done);
+        if (pcg_done) {
+            nrr_b200::pcg_forget_event(pcg_done);
+            cudaEventDestroy(pcg_done);
+        }
         for (auto& x : flush_ev) cudaEventDestroy(x);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
@@ -1013,7 +1018,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
         c->launches += 2;
     }
     if (fresh_sub) NRR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->join, 0));
-    launch_pcg(c->plan, a, c->stream);
+    launch_pcg(c->plan, a, c->stream, c->pcg_done);
     ++c->launches;
 }
 
@@ -1347,6 +1352,7 @@ int nrr_ctx_create(int device, nrr_ctx** out) {
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->eval_done, cudaEventDisableTiming));
         NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->end_done, cudaEventDisableTiming));
+        NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->pcg_done, cudaEventDisableTiming));
         c->d_rec.resize(1);
         c->d_status.resize(1);
         c->deg.resize(1);
