@@ -424,6 +424,35 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->src_avg = p->src_avg_edge_length;
     c->h_src.assign(p->source, p->source + 3 * static_cast<size_t>(n));
     const int sumk = n > 0 ? p->infl_offsets[n] : 0;
+    if (sumk < 0) throw ConfigError("negative influence count");
+    // the caller's arrays go to the device on a helper thread while this one
+    // builds the plan (pageable copies block the issuing thread); joined before
+    // the device setup that reads them, and on any exception
+    struct Joiner {
+        std::thread t;
+        std::exception_ptr err;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+        void join() {
+            if (t.joinable()) t.join();
+            if (err) std::rethrow_exception(err);
+        }
+    } uploader;
+    uploader.t = std::thread([c, p, n, N, P, sumk, s, &uploader] {
+        try {
+            NRR_CUDA_CHECK(cudaSetDevice(c->device));
+            c->d_src.upload(p->source, 3 * static_cast<size_t>(n), s);
+            c->d_infl_off.upload(p->infl_offsets, n + 1, s);
+            c->d_infl_node.upload(p->infl_nodes, sumk, s);
+            c->d_infl_w.upload(p->infl_weights, sumk, s);
+            c->d_node_pos.upload(p->node_positions, 3 * static_cast<size_t>(N), s);
+            c->d_pairs.upload(p->reg_pairs, 2 * static_cast<size_t>(P), s);
+            c->d_pair_c.upload(p->reg_weights, P, s);
+        } catch (...) {
+            uploader.err = std::current_exception();
+        }
+    });
     // influence validation (the constants w [v - p; 1] and sum w p are built
     // on the device, setup_gpu.cu); entries per vertex for the contributor lists
     std::vector<long long> pair_off(static_cast<size_t>(n) + 1, 0);
@@ -534,17 +563,11 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     }
     if (P == 0 && E > 0) throw ConfigError("graph edges without reg pairs");
     clk.lap("pairs");
-    // upload
-    c->d_src.upload(p->source, 3 * static_cast<size_t>(n), s);
-    c->d_infl_off.upload(p->infl_offsets, n + 1, s);
-    c->d_infl_node.upload(p->infl_nodes, sumk, s);
-    c->d_infl_w.upload(p->infl_weights, sumk, s);
+    // upload (the caller's arrays: on the helper thread)
+    uploader.join();
     c->d_infl_f.resize(std::max(sumk, 1));
     c->d_anchor.resize(std::max<size_t>(3 * static_cast<size_t>(n), 1));
     c->h_anchor.clear();  // downloaded on demand (nrr_assemble)
-    c->d_node_pos.upload(p->node_positions, 3 * static_cast<size_t>(N), s);
-    c->d_pairs.upload(p->reg_pairs, 2 * static_cast<size_t>(P), s);
-    c->d_pair_c.upload(p->reg_weights, P, s);
     c->d_pair_rev.upload(rev.data(), P, s);
     {  // g_e = c [p_i - p_j; 1] per directed pair (energy.hpp:163-173)
         std::vector<double4> gv(std::max(P, 1));
