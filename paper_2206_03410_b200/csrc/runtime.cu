@@ -488,19 +488,30 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     if (entries >= (1LL << 31)) throw ConfigError("assembly contributor lists exceed 2^31 entries");
     clk.lap("influence constants");
     // BSR pattern: diagonal + both halves of each edge (energy.hpp:264-279)
-    std::vector<std::vector<int>> cols(N);
-    for (int j = 0; j < N; ++j) cols[j].push_back(j);
+    // flat CSR by counting (the node itself + both ends of every edge), then
+    // each row sorted and deduplicated
+    std::vector<int> coff(static_cast<size_t>(N) + 1, 0);
+    for (int j = 0; j < N; ++j) coff[j + 1] = 1;
     for (int e = 0; e < E; ++e) {
         const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
         if (a < 0 || b < 0 || a >= N || b >= N || a == b) throw ConfigError("graph edge index out of range");
-        cols[a].push_back(b);
-        cols[b].push_back(a);
+        ++coff[a + 1];
+        ++coff[b + 1];
+    }
+    for (int j = 0; j < N; ++j) coff[j + 1] += coff[j];
+    std::vector<int> cflat(coff[N]), cfill(coff.begin(), coff.end() - 1);
+    for (int j = 0; j < N; ++j) cflat[cfill[j]++] = j;
+    for (int e = 0; e < E; ++e) {
+        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
+        cflat[cfill[a]++] = b;
+        cflat[cfill[b]++] = a;
     }
     std::vector<int> deg(N);
     for (int j = 0; j < N; ++j) {
-        std::sort(cols[j].begin(), cols[j].end());
-        cols[j].erase(std::unique(cols[j].begin(), cols[j].end()), cols[j].end());
-        deg[j] = static_cast<int>(cols[j].size());
+        int* lo = cflat.data() + coff[j];
+        int* hi = cflat.data() + coff[j + 1];
+        std::sort(lo, hi);
+        deg[j] = static_cast<int>(std::unique(lo, hi) - lo);
     }
     // solver row order: RCB subdomains, one per CTA (pcg.cu)
     clk.lap("pattern");
@@ -512,7 +523,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     for (int r = 0; r < N; ++r) {
         const int j = c->plan.row_node[r];
         c->h_row_ptr[r + 1] = c->h_row_ptr[r] + deg[j];
-        c->h_col.insert(c->h_col.end(), cols[j].begin(), cols[j].end());
+        c->h_col.insert(c->h_col.end(), cflat.begin() + coff[j], cflat.begin() + coff[j] + deg[j]);
     }
     const int nnzb = c->h_row_ptr[N];
     auto find_blk = [&](int a, int b) -> int {
@@ -549,17 +560,33 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
             if (p->reg_pairs[2 * e + 1] == j) return e;
         return -1;
     };
-    for (int e = 0; e < P; ++e) {
-        rev[e] = pair_index(p->reg_pairs[2 * e + 1], p->reg_pairs[2 * e]);
-        if (rev[e] < 0) throw ConfigError("reg pairs are not symmetric");
-    }
-    for (int e = 0; e < E; ++e) {
-        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
-        kpos[N + e] = find_blk(a, b);
-        kpos_t[N + e] = find_blk(b, a);
-        eab[e] = pair_index(a, b);
-        eba[e] = pair_index(b, a);
-        if ((eab[e] < 0 || eba[e] < 0) && P > 0) throw ConfigError("graph edge without reg pairs");
+    {  // reverse pairs and per-edge positions on host threads (independent entries)
+        const int T = std::max(1, std::min<int>(8, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<int> bad(T, 0);
+        auto part = [&](int t) {
+            for (int e = static_cast<int>(static_cast<long long>(P) * t / T);
+                 e < static_cast<int>(static_cast<long long>(P) * (t + 1) / T); ++e) {
+                rev[e] = pair_index(p->reg_pairs[2 * e + 1], p->reg_pairs[2 * e]);
+                if (rev[e] < 0) bad[t] |= 1;
+            }
+            for (int e = static_cast<int>(static_cast<long long>(E) * t / T);
+                 e < static_cast<int>(static_cast<long long>(E) * (t + 1) / T); ++e) {
+                const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
+                kpos[N + e] = find_blk(a, b);
+                kpos_t[N + e] = find_blk(b, a);
+                eab[e] = pair_index(a, b);
+                eba[e] = pair_index(b, a);
+                if ((eab[e] < 0 || eba[e] < 0) && P > 0) bad[t] |= 2;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; ++t) th.emplace_back(part, t);
+        part(0);
+        for (auto& x : th) x.join();
+        int b = 0;
+        for (int v : bad) b |= v;
+        if (b & 1) throw ConfigError("reg pairs are not symmetric");
+        if (b & 2) throw ConfigError("graph edge without reg pairs");
     }
     if (P == 0 && E > 0) throw ConfigError("graph edges without reg pairs");
     clk.lap("pairs");
