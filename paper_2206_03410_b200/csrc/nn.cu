@@ -196,6 +196,24 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             best_i = p;
         }
     }
+    if (best_d2 == INFINITY && bv.gpts != nullptr) {
+        // no seed: any point of the query's own cell (if it has one) gives a
+        // bound, usually tight enough for the grid path below
+        const int ix = static_cast<int>(floorf((fx - bv.glx) * bv.inv_h));
+        const int iy = static_cast<int>(floorf((fy - bv.gly) * bv.inv_h));
+        const int iz = static_cast<int>(floorf((fz - bv.glz) * bv.inv_h));
+        if (ix >= 0 && ix < bv.gnx && iy >= 0 && iy < bv.gny && iz >= 0 && iz < bv.gnz) {
+            const int cell = (ix * bv.gny + iy) * bv.gnz + iz;
+            const int p0 = bv.cell_start[cell];
+            if (p0 < bv.cell_start[cell + 1]) {
+                int idx;
+                const float w = bv.gpts[p0].w;
+                memcpy(&idx, &w, 4);
+                best_d2 = exact_d2(bv.tgt64 + 3 * idx, qx, qy, qz);
+                best_i = idx;
+            }
+        }
+    }
     // ---- grid path: a warm-started query whose search ball covers at most
     // kGridCells cells scans those cells (8 lanes round-robin over them);
     // every point within the bound lies in one of them (cells partition space)
