@@ -434,3 +434,25 @@ def test_step_parity_large_subdomains(cap):
         assert err <= 1e-8 * (1 + np.max(np.abs(o["Xmm"]))), err
     finally:
         c.close()
+
+
+def test_cluster_resident_pcg_step_parity(monkeypatch, strip):
+    """The opt-in cluster-resident solver (NRR_PCG=cluster: one thread-block
+    cluster, K in distributed shared memory) solves the same teacher-forced
+    pass to the reference bar."""
+    monkeypatch.setenv("NRR_PCG", "cluster")
+    c = R.Context()
+    try:
+        c.set_problem(strip)
+        c.set_target(strip.target)
+        N = strip.graph.node_count
+        row_ptr, _ = R.bsr_pattern(strip.graph)
+        nnzb = int(row_ptr[-1])
+        X = random_transforms(N, 9, 0.1)
+        prm = (0.8, 1.7, 0.09, 0.12)
+        g = c.step(X, prm, nnzb=nnzb)
+        o = O.step(strip, X, prm, nnzb)
+        err = np.max(np.abs(g["Xmm"] - o["Xmm"]))
+        assert err <= 1e-8 * (1 + np.max(np.abs(o["Xmm"]))), err
+    finally:
+        c.close()
