@@ -23,6 +23,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                   "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
+# extra defines for development builds, e.g. NRR_BUILD_DEFINES="-DNRR_PCG_PROBES=1"
+# (per-iteration PCG phase probes, printed with NRR_PROF=1)
+CUFLAGS += os.environ.get("NRR_BUILD_DEFINES", "").split()
 CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE, "-I", CSRC,
             "-I", "/usr/local/cuda/include"]
 

@@ -51,6 +51,12 @@ namespace nrr_b200 {
 namespace {
 
 constexpr int kQ = kPcgSlots;  // partial slots per CTA and phase
+// per-iteration clock64 phase probes (NRR_PROF=1 prints them); compiled out
+// unless built with -DNRR_PCG_PROBES=1 (they cost issue slots in the loop)
+#ifndef NRR_PCG_PROBES
+#define NRR_PCG_PROBES 0
+#endif
+constexpr bool kPcgProbes = NRR_PCG_PROBES != 0;
 constexpr int kCoarseThreads = 512;
 
 // coarse mode k of node a in aggregate g: [e_k; d_k] for k < 3, e_3 for k = 3,
@@ -1137,7 +1143,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     long long tp = clock64(), acc_t[16] = {0};
     const long long t_setup = tp - t_entry;
     auto mark = [&](int slot) {
-        if (prof) {
+        if (kPcgProbes && prof) {
             const long long t = clock64();
             acc_t[slot] += t - tp;
             tp = t;
@@ -1273,10 +1279,10 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     const bool cprof = a.cta_prof != nullptr && threadIdx.x == 0;
     long long cw[3] = {0, 0, 0}, ct = 0;
     auto cstart_t = [&]() {
-        if (cprof) ct = clock64();
+        if (kPcgProbes && cprof) ct = clock64();
     };
     auto cstop_t = [&](int k) {
-        if (cprof) cw[k] += clock64() - ct;
+        if (kPcgProbes && cprof) cw[k] += clock64() - ct;
     };
 
     while (true) {
