@@ -319,7 +319,11 @@ void harvest(nrr_ctx* c, const bool ran[nrr_ctx::kClasses]) {
     for (int k = 0; k < nrr_ctx::kClasses; ++k) {
         if (!ran[k]) continue;
         float ms = 0.f;
+        // a class whose events were not recorded (timing switched on between
+        // a queued evaluation and its harvest) is skipped, and its error
+        // cleared so a later launch check does not report it
         if (cudaEventElapsedTime(&ms, c->ev[k][0], c->ev[k][1]) == cudaSuccess) c->class_ms[k] += ms;
+        else (void)cudaGetLastError();
     }
 }
 

@@ -12,6 +12,7 @@ ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--max-ctas", type=int, default=0)
+ap.add_argument("--no-timing", action="store_true")
 a = ap.parse_args()
 p = R.make_problem(a.config, scale=a.scale)
 ctx = R.Context(max_ctas=a.max_ctas)
@@ -19,7 +20,7 @@ ctx.set_problem(p)
 prm = ctx.init_parameters()
 cfg = R.solver_config(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300,
                       i_max=a.warmup + a.iters + 5)
-ctx.enable_timing(True)
+ctx.enable_timing(not a.no_timing)
 ctx.begin(cfg)
 ctx.iterate(a.warmup)
 s0 = ctx.stats()
