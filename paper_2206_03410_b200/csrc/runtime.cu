@@ -251,7 +251,7 @@ struct nrr_ctx {
     DevBuf<PcgStatus> d_status;
     DevBuf<PassRecord> d_rec;
     Pinned<PassRecord> h_rec, h_rec_end;
-    Pinned<PcgStatus> h_status;
+    Pinned<PcgStatus> h_status, h_status_init;  // init: constant {no failure}, copied before every solve
     Pinned<int> h_deg;
     // Anderson
     int aa_m = 0;
@@ -982,8 +982,9 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     ClassTimer t(c, kPcg);
     if (xout != x0)
         NRR_CUDA_CHECK(cudaMemcpyAsync(xout, x0, sizeof(double) * 12 * c->N, cudaMemcpyDeviceToDevice, c->stream));
-    PcgStatus init{0x7fffffff, 0, 0, 0, 0.0};
-    NRR_CUDA_CHECK(cudaMemcpyAsync(c->d_status.p, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    *c->h_status_init.p = PcgStatus{0x7fffffff, 0, 0, 0, 0.0};  // pinned: the copy stays asynchronous
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->d_status.p, c->h_status_init.p, sizeof(PcgStatus), cudaMemcpyHostToDevice,
+                                   c->stream));
     PcgArgs a{};
     a.row_ptr = c->d_row_ptr.p;
     a.col = c->d_col.p;
