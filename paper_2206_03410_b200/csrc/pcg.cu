@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     // local memory).
     const int nel = nrows * 12;
     const int my_rc = threadIdx.x % 12, my_r = my_rc / 3, my_c = my_rc % 3;
-    double xr[EPT], br[EPT], rr[EPT], ur[EPT], wr[EPT], pr[EPT], sr[EPT], qr[EPT], zv[EPT];
+    double xr[EPT], rr[EPT], ur[EPT], wr[EPT], pr[EPT], sr[EPT], qr[EPT], zv[EPT];  // B is re-read at a restart
     int el_row[EPT], el_b0[EPT], el_b1[EPT];  // row, block range in the CTA's K
     size_t el_g[EPT];
 #pragma unroll
@@ -1033,7 +1033,6 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         el_b1[k] = live ? a.row_ptr[r0 + lr + 1] - kb0 : el_b0[k];
         el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + my_rc;
         xr[k] = live ? a.X[el_g[k]] : 0.0;
-        br[k] = live ? a.B[el_g[k]] : 0.0;
         rr[k] = ur[k] = wr[k] = pr[k] = sr[k] = qr[k] = zv[k] = 0.0;
     }
 
@@ -1299,10 +1298,11 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             double rmx = 0.0, bmx = 0.0, ps[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
-                rr[k] = br[k] - spmv(k);
+                const double bk = el_row[k] >= 0 ? __ldg(a.B + el_g[k]) : 0.0;
+                rr[k] = bk - spmv(k);
                 if (el_row[k] < 0) continue;
                 rmx = fmax(rmx, fabs(rr[k]));
-                bmx = fmax(bmx, fabs(br[k]));
+                bmx = fmax(bmx, fabs(bk));
                 psi_acc(k, rr[k], ps);
             }
             zero_vals();
