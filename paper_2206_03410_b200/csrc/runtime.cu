@@ -182,6 +182,13 @@ struct nrr_ctx {
     int nranks = 1, rank = 0, n_global = -1;
     cudaStream_t side = nullptr;  // subdomain inverses run beside the coarse setup
     cudaEvent_t fork = nullptr, join = nullptr;
+    // side-by-side mode (opt.max_ctas > 0) with NRR_PCG_PRIORITY set: the
+    // cooperative PCG grid runs on a greatest-priority stream so its pending
+    // CTAs take SMs ahead of the short kernels of the neighbouring contexts as
+    // they free (a mitigation candidate for the config-3 hang, DESIGN.md;
+    // ~10% slower on config 3, so off by default)
+    cudaStream_t pcg_stream = nullptr;
+    cudaEvent_t pcg_fork = nullptr;
     int num_sms = 0;
     size_t smem_optin = 0;
     nrr_solve_options opt{1e-13, 20000, 0, 0};
@@ -293,6 +300,8 @@ struct nrr_ctx {
             cudaEventDestroy(pcg_done);
         }
         for (auto& x : flush_ev) cudaEventDestroy(x);
+        if (pcg_fork) cudaEventDestroy(pcg_fork);
+        if (pcg_stream) cudaStreamDestroy(pcg_stream);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -1072,8 +1081,22 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
         launch_coarse_setup(c->plan, a, CoarseWork{c->coarse_part.p, c->coarse_inv.p}, c->stream);
         c->launches += 2;
     }
-    if (fresh_sub) NRR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->join, 0));
-    launch_pcg(c->plan, a, c->stream, c->pcg_done);
+    if (c->opt.max_ctas > 0 && std::getenv("NRR_PCG_PRIORITY")) {
+        if (!c->pcg_stream) {
+            int lo = 0, hi = 0;
+            NRR_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            NRR_CUDA_CHECK(cudaStreamCreateWithPriority(&c->pcg_stream, cudaStreamNonBlocking, hi));
+            NRR_CUDA_CHECK(cudaEventCreateWithFlags(&c->pcg_fork, cudaEventDisableTiming));
+        }
+        NRR_CUDA_CHECK(cudaEventRecord(c->pcg_fork, c->stream));
+        NRR_CUDA_CHECK(cudaStreamWaitEvent(c->pcg_stream, c->pcg_fork, 0));
+        if (fresh_sub) NRR_CUDA_CHECK(cudaStreamWaitEvent(c->pcg_stream, c->join, 0));
+        launch_pcg(c->plan, a, c->pcg_stream, c->pcg_done);
+        NRR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->pcg_done, 0));
+    } else {
+        if (fresh_sub) NRR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->join, 0));
+        launch_pcg(c->plan, a, c->stream, c->pcg_done);
+    }
     ++c->launches;
 }
 
