@@ -373,12 +373,17 @@ def _fixed_count_run(p, iters, max_ctas=0):
         c.close()
 
 
-def test_side_by_side_contexts_match_sequential():
+@pytest.mark.parametrize("priority", [False, True])
+def test_side_by_side_contexts_match_sequential(priority, monkeypatch):
     """Config 3 runs several registrations at once (one context, stream and
     host thread each, PCG grid capped): every pair must produce bitwise the
     result it produces alone with the same grid cap, and the energies of an
-    uncapped run within the parity band (the PCG partition differs)."""
+    uncapped run within the parity band (the PCG partition differs). With
+    NRR_PCG_PRIORITY the PCG grids run on greatest-priority streams."""
     import threading
+
+    if priority:
+        monkeypatch.setenv("NRR_PCG_PRIORITY", "1")
 
     probs = [R.make_problem(3, seed=4000 + q, scale=0.25) for q in range(4)]
     alone = [_fixed_count_run(p, 12, max_ctas=24) for p in probs]
