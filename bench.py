@@ -162,7 +162,7 @@ class ClockSampler:
 # ----------------------------------------------------------------- workload
 def problem_for(config, rank=0):
     from paper_2206_03410_b200 import registration as R
-    if config == 3:  # one pair of the batch (reference arm / CPU sample)
+    if config == 3:  # one pair of the batch
         return R.make_problem(3, seed=4000)
     return R.make_problem(config)
 
@@ -215,6 +215,21 @@ def h2d_d2h_bytes(p):
     return int(h2d), int(d2h)
 
 
+def host_cpu():
+    """Core count and CPU model of the host this runs on (the GPU box in a
+    driver run)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def cpu_baseline(p, cfg_kw, warmup, steps):
     from oracle import binding as O
     cfg = O.config(**cfg_kw)
@@ -222,32 +237,79 @@ def cpu_baseline(p, cfg_kw, warmup, steps):
     return steps / sec, sec
 
 
+def reference_pairs(args, threads):
+    """Config 3 on the CPU: independent pairs on `threads` host threads (the
+    reference's model: one registration per thread, README.md:217-219); a
+    bounded sample of 2 pairs per thread, each the full 50-iteration
+    fixed-count run. Returns (iterations/s, pairs, seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import binding as O
+    npairs = min(args.pairs, 2 * threads)
+    probs = [O.make_problem(3, seed=4000 + q) for q in range(npairs)]
+    cfgs = []
+    for p in probs:
+        prm = O.init_parameters(p)
+        cfgs.append(O.config(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300))
+
+    def one(k):
+        return O.time_iterations(probs[k], cfgs[k], 0, args.pair_iters)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(npairs)))
+    wall = time.perf_counter() - t0
+    return npairs * args.pair_iters / wall, npairs, wall
+
+
 def run_reference(args, dist):
-    """The reference's own CPU implementation of the path: the unbuildable
-    Eigen reference is replaced by its restatement (oracle/), single thread
-    per registration as the reference (README.md:217-219)."""
+    """--impl reference: the reference's own CPU implementation of the path.
+    The Eigen reference cannot be built here, so its restatement
+    (oracle/, single thread per registration as the reference,
+    README.md:217-219) is timed on the box's host cores. Its inputs come from
+    the oracle alone (oracle.binding.make_problem: the same seeded arrays,
+    tests/test_inputs.py), so this process never loads libnrr_b200.so. Same
+    config, steps and warm-up as the GPU arm, except config 4, where one
+    iteration of the reference (a 70K-unknown direct solve) takes ~45 s and
+    the sample is capped at 3 timed iterations after 1 warm-up."""
     if dist.rank != 0:
         dist.barrier()
         dist.close()
         return
     from oracle import binding as O
-    p = problem_for(args.config)
-    prm = O.init_parameters(p)
-    kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300)
-    steps = max(1, min(args.steps, 10))
-    warm = max(1, min(args.warmup, 3))
-    value, sec = cpu_baseline(p, kw, warm, steps)
-    g = p.graph
+    host = host_cpu()
+    if args.config == 3:
+        threads = host["nproc"] or 1
+        value, npairs, sec = reference_pairs(args, threads)
+        steps, warm = args.pair_iters, 0
+        cores = threads
+        sample = (f"{npairs} pairs x {args.pair_iters} fixed-count iterations on {threads} threads (one pair per "
+                  "thread at a time); value = their iterations / wall time")
+        workload = f"config 3: pairs of 20K source points (~600 nodes), {args.pair_iters} fixed-count iterations each"
+        ms = 1e3 * sec / (npairs * args.pair_iters)
+    else:
+        p = O.make_problem(args.config)
+        prm = O.init_parameters(p)
+        kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300)
+        steps, warm = args.steps, max(3, args.warmup)
+        if args.config == 4:
+            steps, warm = min(steps, 3), 1
+        value, sec = cpu_baseline(p, kw, warm, steps)
+        cores = 1
+        g = p.graph
+        sample = (f"{steps} accepted MM iterations after {warm} warm-up, one registration on one thread "
+                  "(the reference is single-threaded)")
+        workload = (f"config {args.config}: {p.n} source / {len(p.target)} target points, {g.node_count} nodes, "
+                    "fixed-count single stage (nu fixed, eps=1e-300), AA m=5")
+        ms = 1e3 * sec / steps
     line = {
         "impl": "reference", "metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * sec / steps, "higher_is_better": True,
+        "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config {args.config}: {p.n} source / {len(p.target)} target points, "
-                               f"{g.node_count} nodes, fixed-count single stage",
-                   "sample": f"{steps} MM iterations after {warm} warm-up"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{steps} MM iterations of config {args.config} after {warm} warm-up, "
-                                   "oracle restatement (reference needs Eigen, absent)"},
+        "config": {"workload": workload, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "host": host,
+                         "note": "oracle restatement of the reference (the Eigen reference is unbuildable here)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -355,7 +417,7 @@ def run_b200(args, dist):
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         cps, sec = cpu_baseline(p, cfg_kw, 1, args.cpu_steps)
-        cpu = {"value": cps, "unit": UNIT, "cores": 1, "kind": "port",
+        cpu = {"value": cps, "unit": UNIT, "cores": 1, "kind": "port", "host": host_cpu(),
                "sample": f"{args.cpu_steps} MM iterations of config {args.config} (n={n}) after 1 warm-up, "
                          "oracle restatement, one thread (the reference is single-threaded)"}
     if dist.rank == 0:
@@ -511,12 +573,28 @@ def run_pairs(args, dist):
     dist.close()
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: launch the N ranks ourselves (one
+    process per GPU, rendezvous on 127.0.0.1) and relay rank 0's line."""
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     if os.environ.get("BENCH_TRACEBACK_AFTER"):  # debugging aid: dump all thread stacks after N seconds
         import faulthandler
 
         faulthandler.dump_traceback_later(float(os.environ["BENCH_TRACEBACK_AFTER"]), exit=True)
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     dist = Dist()
     if args.impl == "reference":
         run_reference(args, dist)

@@ -101,7 +101,7 @@ typedef struct nrr_report_summary {
 typedef struct nrr_solve_options {
     double pcg_rtol;      /* default 1e-13: AA trajectories then track the reference as long as the reference tracks itself under a change of direct-solver ordering */
     int32_t pcg_max_iter; /* default 20000 */
-    int32_t record_passes;/* keep per-pass records (and NN indices if nonzero==2) */
+    int32_t record_passes;/* keep per-pass records: 1 = records, 2 = + NN indices, 3 = + pass trace (nrr_ctx_trace) */
     int32_t max_ctas;     /* PCG grid cap, 0 = one CTA per SM; set before nrr_ctx_set_problem. Several contexts
                              driven from several host threads then run side by side (config 3 batches) */
 } nrr_solve_options;
@@ -163,6 +163,24 @@ int nrr_ctx_set_shard(nrr_ctx* ctx, int32_t n_global);
 int nrr_ctx_report(nrr_ctx* ctx, nrr_report_summary* summary, nrr_stage_record* stages,
                    int32_t stage_cap, nrr_iteration_record* iters, int32_t iter_cap,
                    nrr_pass_record* passes, int32_t pass_cap, int32_t* pass_nn_index);
+
+/* Pass trace (test instrumentation; set nrr_solve_options.record_passes = 3
+ * before nrr_ctx_begin): every evaluated pass of the last run in order —
+ * reverted ones included — with the iterate it was evaluated at (X, 12N
+ * column-major), its correspondences (n target indices), its energies, and,
+ * for an accepted pass, the solve's x_mm (12N column-major; NaN otherwise).
+ * Lets a caller re-run the reference step at every iterate of the device
+ * trajectory (teacher-forced parity of solver.hpp:224-289). */
+typedef struct nrr_pass_trace {
+    double e_align, e_reg, e_rot, e_total, e_landmark;
+    double max_disp;          /* accepted passes: max |v' - v| of the next iterate */
+    int32_t stage, reverted;  /* reverted: the safeguard (solver.hpp:239) rejected the iterate */
+    int32_t pcg_iterations;   /* accepted passes */
+    int32_t accepted_index;   /* index of its IterationRecord, -1 for a reverted pass */
+} nrr_pass_trace;
+int nrr_ctx_trace_count(nrr_ctx* ctx, int32_t* passes);
+int nrr_ctx_trace(nrr_ctx* ctx, int32_t pass, nrr_pass_trace* rec, double* x_eval, double* x_mm,
+                  int32_t* nn_index);
 
 /* SpatialIndex::nearest / find_correspondences (kd_tree.hpp:124-129,
  * energy.hpp:28-42) for a batch of host queries; out_distance = sqrt(d2). */

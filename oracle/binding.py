@@ -5,6 +5,7 @@ __graft_entry__.smoke() and bench.py's CPU-baseline legs, as the checker.
 import ctypes as C
 import os
 import subprocess
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -289,3 +290,91 @@ def time_iterations(problem, cfg, warmup, steps):
     s = C.c_double()
     _check(lib.oracle_time_iterations(C.byref(v), C.byref(cfg), warmup, steps, C.byref(s)))
     return s.value
+
+
+# ---------------------------------------------------------------- inputs
+# Radius multipliers of the synthetic configs (R = mult * mean edge length),
+# the same table as paper_2206_03410_b200.registration.GRAPH_MULT (a CPU test
+# keeps them equal): the reference arm builds its inputs from the oracle
+# alone, without loading the product library.
+GRAPH_MULT = {0: 5.0, 1: 5.5, 2: 5.0, 3: 5.9, 4: 7.2}
+
+
+@dataclass
+class Graph:
+    """DeformationGraph (deformation_graph.hpp:50-67) as flat arrays."""
+    node_indices: np.ndarray
+    node_positions: np.ndarray
+    edges: np.ndarray
+    infl_offsets: np.ndarray
+    infl_nodes: np.ndarray
+    infl_weights: np.ndarray
+    infl_dist: np.ndarray
+    reg_pairs: np.ndarray
+    reg_weights: np.ndarray
+    radius: float = 0.0
+
+    @property
+    def node_count(self):
+        return len(self.node_indices)
+
+    @property
+    def pair_count(self):
+        return len(self.reg_weights)
+
+
+@dataclass
+class Problem:
+    source: np.ndarray
+    target: np.ndarray
+    graph: Graph
+    src_avg_edge_length: float
+    faces: object = None
+
+    @property
+    def n(self):
+        return len(self.source)
+
+
+def synth(config, seed=None, scale=1.0):
+    lib = load()
+    if seed is None:
+        seed = 1000 * (config + 1)
+    n, nf, m = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib.oracle_synth_config(config, C.c_uint64(seed), C.c_double(scale), C.byref(n), C.byref(nf), C.byref(m),
+                                   None, None, None))
+    src, faces, tgt = np.zeros((n.value, 3)), np.zeros((nf.value, 3), np.int32), np.zeros((m.value, 3))
+    _check(lib.oracle_synth_config(config, C.c_uint64(seed), C.c_double(scale), C.byref(n), C.byref(nf), C.byref(m),
+                                   _d(src), _i(faces), _d(tgt)))
+    return src, (faces if nf.value else None), tgt
+
+
+def normalize_pair(source, target):
+    lib = load()
+    s, t = _f64(source).reshape(-1, 3).copy(), _f64(target).reshape(-1, 3).copy()
+    out = np.zeros(4)
+    _check(lib.oracle_normalize_pair(_d(s), len(s), _d(t), len(t), _d(out)))
+    return s, t, out[0], out[1:4].copy()
+
+
+def avg_edge_length(points, edges):
+    lib = load()
+    p, e = _f64(points).reshape(-1, 3), _i32(edges).reshape(-1, 2)
+    out = C.c_double()
+    _check(lib.oracle_avg_edge_length(_d(p), len(p), _i(e), len(e), C.byref(out)))
+    return out.value
+
+
+def make_problem(config, seed=None, scale=1.0, mult=None):
+    """The synthetic pair of BASELINE config `config` built by the oracle alone
+    (synth -> normalize_pair -> edges -> build_graph, surface.hpp /
+    deformation_graph.hpp restated): the same arrays as
+    paper_2206_03410_b200.registration.make_problem (tests/test_oracle_kats.py
+    checks bitwise equality)."""
+    src, faces, tgt = synth(config, seed, scale)
+    src, tgt, _, _ = normalize_pair(src, tgt)
+    edges = edges_from_faces(faces, len(src)) if faces is not None else knn_edges(src, 6)
+    lbar = avg_edge_length(src, edges)
+    radius = (GRAPH_MULT[config] if mult is None else mult) * lbar
+    g = build_graph(src, edges, radius)
+    return Problem(src, tgt, Graph(radius=radius, **g), lbar, faces)

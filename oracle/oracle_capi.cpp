@@ -1,5 +1,6 @@
 // ORACLE — TEST INFRASTRUCTURE ONLY. extern "C" layer over nrr_oracle.hpp.
 #include "oracle_capi.h"
+#include "nrr_synth.hpp"
 
 #include <cstring>
 #include <exception>
@@ -134,6 +135,40 @@ int oracle_avg_edge_length(const double* pts, int32_t n, const int32_t* edges, i
         for (int e = 0; e < ne; ++e) s.edges.emplace_back(edges[2 * e], edges[2 * e + 1]);
         s.finalize_edges();
         *out = s.avg_edge_length;
+    });
+}
+
+int oracle_normalize_pair(double* src, int32_t n, double* tgt, int32_t m, double* out4) {
+    return guard([&] {
+        Surface s, t;
+        s.points = to_vec3(src, n);
+        t.points = to_vec3(tgt, m);
+        const Normalization nm = normalize_pair(s, t);
+        for (int i = 0; i < n; ++i)
+            for (int c = 0; c < 3; ++c) src[3 * i + c] = s.points[i][c];
+        for (int i = 0; i < m; ++i)
+            for (int c = 0; c < 3; ++c) tgt[3 * i + c] = t.points[i][c];
+        out4[0] = nm.scale;
+        for (int c = 0; c < 3; ++c) out4[1 + c] = nm.center[c];
+    });
+}
+
+int oracle_synth_config(int32_t which, uint64_t seed, double scale, int32_t* n, int32_t* nf_src, int32_t* m,
+                        double* src, int32_t* src_faces, double* tgt) {
+    return guard([&] {
+        std::vector<double> s, t;
+        std::vector<int32_t> f;
+        try {
+            nrr_synth::synth_config(which, seed, scale, s, f, t);
+        } catch (const std::invalid_argument& e) {
+            throw ConfigError(e.what());
+        }
+        *n = static_cast<int32_t>(s.size() / 3);
+        *nf_src = static_cast<int32_t>(f.size() / 3);
+        *m = static_cast<int32_t>(t.size() / 3);
+        if (src) std::copy(s.begin(), s.end(), src);
+        if (src_faces) std::copy(f.begin(), f.end(), src_faces);
+        if (tgt) std::copy(t.begin(), t.end(), tgt);
     });
 }
 

@@ -77,6 +77,15 @@ void oracle_graph_export(const oracle_graph* g, int32_t* node_indices, double* n
                          double* reg_weights);
 void oracle_graph_free(oracle_graph* g);
 
+/* normalize_pair (surface.hpp:125-149), in place; out4 = {scale, cx, cy, cz} */
+int oracle_normalize_pair(double* src, int32_t n, double* tgt, int32_t m, double* out4);
+/* seeded synthetic inputs of BASELINE configs 0-4 (synth/nrr_synth.hpp, shared
+ * with the product's nrr_synth_config): lets the bench's reference arm build
+ * its inputs without loading the product library. Sizes first with NULL
+ * buffers. */
+int oracle_synth_config(int32_t which, uint64_t seed, double scale, int32_t* n, int32_t* nf_src, int32_t* m,
+                        double* src, int32_t* src_faces, double* tgt);
+
 /* primitives */
 int oracle_nearest(const double* target, int32_t m, const double* queries, int32_t q,
                    int32_t* out_index, double* out_distance);

@@ -18,15 +18,16 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libnrr_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
+SYNTH = os.path.join(ROOT, "synth")  # seeded input generators (shared with the oracle)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                  "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
+                  "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC, "-I", SYNTH]
 # extra defines for development builds, e.g. NRR_BUILD_DEFINES="-DNRR_PCG_PROBES=1"
 # (per-iteration PCG phase probes, printed with NRR_PROF=1)
 CUFLAGS += os.environ.get("NRR_BUILD_DEFINES", "").split()
-CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE, "-I", CSRC,
+CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE, "-I", CSRC, "-I", SYNTH,
             "-I", "/usr/local/cuda/include"]
 
 
@@ -41,6 +42,7 @@ def _sources():
 def _headers():
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
     hs.append(os.path.join(INCLUDE, "nrr_cuda.h"))
+    hs.append(os.path.join(SYNTH, "nrr_synth.hpp"))
     return hs
 
 

@@ -83,6 +83,12 @@ class ReportSummary(C.Structure):
                 ("solve_seconds", C.c_double), ("setup_seconds", C.c_double), ("loop_seconds", C.c_double)]
 
 
+class PassTrace(C.Structure):
+    _fields_ = [("e_align", C.c_double), ("e_reg", C.c_double), ("e_rot", C.c_double), ("e_total", C.c_double),
+                ("e_landmark", C.c_double), ("max_disp", C.c_double), ("stage", C.c_int32),
+                ("reverted", C.c_int32), ("pcg_iterations", C.c_int32), ("accepted_index", C.c_int32)]
+
+
 class SolveOptions(C.Structure):
     _fields_ = [("pcg_rtol", C.c_double), ("pcg_max_iter", C.c_int32), ("record_passes", C.c_int32),
                 ("max_ctas", C.c_int32)]
@@ -103,6 +109,8 @@ _SIGS = {
     "nrr_register": (C.c_int, [C.c_void_p, C.POINTER(ProblemView), C.POINTER(SolverConfig), f64p, f64p]),
     "nrr_ctx_report": (C.c_int, [C.c_void_p, C.POINTER(ReportSummary), C.POINTER(StageRecord), C.c_int32,
                                  C.POINTER(IterationRecord), C.c_int32, C.POINTER(PassRecord), C.c_int32, i32p]),
+    "nrr_ctx_trace_count": (C.c_int, [C.c_void_p, i32p]),
+    "nrr_ctx_trace": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(PassTrace), f64p, f64p, i32p]),
     "nrr_nearest": (C.c_int, [C.c_void_p, f64p, C.c_int32, i32p, f64p]),
     "nrr_nearest_from": (C.c_int, [C.c_void_p, f64p, C.c_int32, i32p, i32p, f64p]),
     "nrr_deform": (C.c_int, [C.c_void_p, f64p, f64p]),

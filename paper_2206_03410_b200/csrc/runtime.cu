@@ -273,6 +273,12 @@ struct nrr_ctx {
     std::vector<nrr_iteration_record> iters;
     std::vector<nrr_pass_record> passes;
     std::vector<int> pass_nn;
+    // pass trace (opt.record_passes >= 3, test instrumentation): per evaluated
+    // pass the iterate it was evaluated at, its correspondences and energies,
+    // and on an accepted pass the solve's x_mm (node-major 12N each)
+    std::vector<nrr_pass_trace> trace;
+    std::vector<double> trace_x, trace_xmm;
+    std::vector<int> trace_nn;
 
     // ---- timing (CUDA events per kernel class)
     static constexpr int kClasses = 6;
@@ -1136,6 +1142,10 @@ void run_begin(nrr_ctx* c, const nrr_solver_config& cfg_in) {
     c->iters.clear();
     c->passes.clear();
     c->pass_nn.clear();
+    c->trace.clear();
+    c->trace_x.clear();
+    c->trace_xmm.clear();
+    c->trace_nn.clear();
     if (c->comm && r.cfg.landmark_count > 0) throw ConfigError("landmarks are not supported on a vertex-sharded run");
     upload_landmarks(c, r.cfg);
     r.prm = init_parameters(c, r.cfg);
@@ -1219,6 +1229,39 @@ void in_pass_flush(nrr_ctx* c) {
     ++c->flush_used;
 }
 
+// ---- pass trace (record_passes >= 3): synchronous copies, test instrumentation only
+void trace_eval(nrr_ctx* c, const PassRecord& e, bool revert) {
+    const size_t D = 12 * static_cast<size_t>(c->N);
+    nrr_pass_trace t{};
+    t.e_align = e.align;
+    t.e_reg = e.reg;
+    t.e_rot = e.rot;
+    t.e_total = e.total;
+    t.e_landmark = e.landmark;
+    t.stage = c->run.si;
+    t.reverted = revert ? 1 : 0;
+    t.accepted_index = -1;
+    c->trace.push_back(t);
+    c->trace_x.resize(c->trace.size() * D);
+    c->trace_xmm.resize(c->trace.size() * D, std::numeric_limits<double>::quiet_NaN());
+    c->trace_nn.resize(c->trace.size() * static_cast<size_t>(c->n));
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->trace_x.data() + (c->trace.size() - 1) * D, c->x.p, sizeof(double) * D,
+                                   cudaMemcpyDeviceToHost, c->stream));
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->trace_nn.data() + (c->trace.size() - 1) * c->n, c->nn_idx.p,
+                                   sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+}
+void trace_accept(nrr_ctx* c, double max_disp) {
+    const size_t D = 12 * static_cast<size_t>(c->N);
+    nrr_pass_trace& t = c->trace.back();
+    t.max_disp = max_disp;
+    t.pcg_iterations = c->h_status.p->iterations;
+    t.accepted_index = static_cast<int32_t>(c->iters.size());
+    NRR_CUDA_CHECK(cudaMemcpyAsync(c->trace_xmm.data() + (c->trace.size() - 1) * D, c->xmm.p, sizeof(double) * D,
+                                   cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+}
+
 // One evaluated pass (solver.hpp:225-288). Returns true when an iteration was
 // accepted; sets *stage_end when the stage converged or hit i_max.
 bool one_pass(nrr_ctx* c, bool* stage_end) {
@@ -1255,6 +1298,7 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     if (!std::isfinite(e_accept)) throw NumericalError("solver aborted: energy is not finite");
     const bool revert = e_accept > r.e_prev && r.current_is_aa;  // solver.hpp:239
     if (c->opt.record_passes) c->passes.push_back({e.total, r.si, revert ? 1 : 0});
+    if (c->opt.record_passes >= 3) trace_eval(c, e, revert);
     if (revert) {  // solver.hpp:244-248 (x_mm of the previous pass is untouched)
         NRR_CUDA_CHECK(cudaMemcpyAsync(c->x.p, c->xmm.p, sizeof(double) * D, cudaMemcpyDeviceToDevice, c->stream));
         deform_run(c, c->x.p, c->vhat.p, nullptr, nullptr);
@@ -1298,6 +1342,7 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     }
     if (c->h_rec_end.p->nonfinite) throw NumericalError("solver aborted: iterate is not finite");
     rec.max_disp = c->h_rec_end.p->max_disp;
+    if (c->opt.record_passes >= 3) trace_accept(c, rec.max_disp);
     c->iters.push_back(rec);
     ++r.st.iteration_count;
     std::swap(c->x.p, c->xnext.p);
@@ -1585,6 +1630,28 @@ int nrr_ctx_report(nrr_ctx* ctx, nrr_report_summary* summary, nrr_stage_record* 
             const size_t cnt = std::min<size_t>(ctx->pass_nn.size(), static_cast<size_t>(pass_cap) * ctx->n);
             std::memcpy(pass_nn_index, ctx->pass_nn.data(), cnt * sizeof(int));
         }
+    });
+}
+
+int nrr_ctx_trace_count(nrr_ctx* ctx, int32_t* passes) {
+    return guarded([&] { *passes = static_cast<int32_t>(ctx->trace.size()); });
+}
+
+int nrr_ctx_trace(nrr_ctx* ctx, int32_t pass, nrr_pass_trace* rec, double* x_eval, double* x_mm, int32_t* nn_index) {
+    return guarded([&] {
+        if (pass < 0 || pass >= static_cast<int32_t>(ctx->trace.size())) throw ConfigError("trace: pass out of range");
+        const int N = ctx->N;
+        const size_t D = 12 * static_cast<size_t>(N);
+        if (rec) *rec = ctx->trace[pass];
+        auto to_col = [&](const double* nm, double* out) {  // x[12j+3r+c] -> X[c*4N + 4j + r]
+            for (int j = 0; j < N; ++j)
+                for (int r = 0; r < 4; ++r)
+                    for (int cc = 0; cc < 3; ++cc)
+                        out[static_cast<size_t>(cc) * 4 * N + 4 * j + r] = nm[12 * static_cast<size_t>(j) + 3 * r + cc];
+        };
+        if (x_eval) to_col(ctx->trace_x.data() + pass * D, x_eval);
+        if (x_mm) to_col(ctx->trace_xmm.data() + pass * D, x_mm);
+        if (nn_index) std::memcpy(nn_index, ctx->trace_nn.data() + static_cast<size_t>(pass) * ctx->n, sizeof(int) * ctx->n);
     });
 }
 

@@ -331,6 +331,25 @@ class Context:
             rep["pass_nn"] = nn
         return rep
 
+    def trace(self):
+        """Pass trace of the last run (record_passes=3): a list of dicts, one per
+        evaluated pass, with the iterate X (12N, reference layout), the NN
+        indices, the energies and, on accepted passes, x_mm."""
+        cnt = C.c_int32()
+        check(self.lib.nrr_ctx_trace_count(self.h, C.byref(cnt)))
+        out = []
+        for k in range(cnt.value):
+            t = capi.PassTrace()
+            X = np.zeros(12 * self.N)
+            Xmm = np.zeros(12 * self.N)
+            nn = np.zeros(self.n, np.int32)
+            check(self.lib.nrr_ctx_trace(self.h, k, C.byref(t), d(X), d(Xmm), i(nn)))
+            out.append({"X": X, "Xmm": Xmm if t.accepted_index >= 0 else None, "index": nn,
+                        "energy": np.array([t.e_align, t.e_reg, t.e_rot, t.e_total]), "E_landmark": t.e_landmark,
+                        "max_disp": t.max_disp, "stage": t.stage, "reverted": bool(t.reverted),
+                        "pcg_iterations": t.pcg_iterations, "accepted_index": t.accepted_index})
+        return out
+
     def nearest(self, queries, prev=None):
         """Exact nearest target (smallest index on ties); `prev` (target
         indices) warm-starts the bound as the registration passes do."""
