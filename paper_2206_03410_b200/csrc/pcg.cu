@@ -1677,7 +1677,12 @@ namespace {
 struct CoopBudget {
     std::mutex mu;
     std::map<int, std::vector<std::pair<cudaEvent_t, int>>> inflight;
-    void acquire(int dev, int ctas, int sms, cudaEvent_t ev) {
+    // Waits until `ctas` more CTAs fit the device's budget and returns with
+    // the mutex held: the caller launches its grid and records `ev` behind
+    // it before calling commit(), so no other thread can query `ev` between
+    // the budget check and the recording (a query of the event's previous,
+    // completed recording would drop a grid that is in flight).
+    std::unique_lock<std::mutex> acquire(int dev, int ctas, int sms, cudaEvent_t ev) {
         std::unique_lock<std::mutex> lk(mu);
         auto& v = inflight[dev];
         // the caller's previous grid has completed (the host synchronised
@@ -1702,8 +1707,10 @@ struct CoopBudget {
             std::this_thread::sleep_for(std::chrono::microseconds(20));
             lk.lock();
         }
-        v.push_back({ev, ctas});
+        return lk;
     }
+    // with the lock from acquire() still held, after cudaEventRecord(ev)
+    void commit(int dev, int ctas, cudaEvent_t ev) { inflight[dev].push_back({ev, ctas}); }
     void forget(cudaEvent_t ev) {
         std::lock_guard<std::mutex> lk(mu);
         for (auto& [d, v] : inflight)
@@ -1758,14 +1765,17 @@ void launch_pcg(const PcgPlan& plan, PcgArgs args, cudaStream_t s, cudaEvent_t d
     // Several contexts may launch their PCG grids side by side (config 3).
     // A grid spins at its barriers, so two partially resident grids could
     // wait on each other's SMs; a per-device budget keeps the sum of the
-    // cooperative grids in flight within one CTA per SM. The budget is
-    // returned by a host callback when the kernel has finished.
+    // cooperative grids in flight within one CTA per SM. A grid's budget
+    // returns when its completion event (recorded right behind it, under the
+    // budget's lock) is found complete by a later acquire's poll.
     int dev = 0, sms = 0;
     NRR_CUDA_CHECK(cudaGetDevice(&dev));
     NRR_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    coop_budget().acquire(dev, plan.grid, sms, done);
+    auto& budget = coop_budget();
+    auto lk = budget.acquire(dev, plan.grid, sms, done);
     NRR_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kPcgThreads), kargs, plan.smem_bytes, s));
     NRR_CUDA_CHECK(cudaEventRecord(done, s));
+    budget.commit(dev, plan.grid, done);
 }
 
 }  // namespace nrr_b200

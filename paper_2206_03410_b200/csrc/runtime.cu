@@ -227,6 +227,11 @@ struct nrr_ctx {
     // last rebuild. Measured on config 2: iterations unchanged, -7% per pass.
     int sub_refresh = 64, coarse_refresh = 64;
     bool last_solve_fresh = false;
+    // the ages before the latest queued solve: a pass the device reverts skips
+    // its solve (and any preconditioner rebuild it asked for), so the host
+    // restores them
+    int prev_sub_age = -1, prev_coarse_age = -1;
+    bool prev_solve_fresh = false;
     int base_iters = 0;
     cudaEvent_t eval_done = nullptr;
     cudaEvent_t end_done = nullptr;
@@ -1073,6 +1078,9 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     // (precond_refresh passes; 1 = rebuild every solve)
     const bool fresh_sub = !c->reuse_precond || c->sub_age < 0 || c->sub_age >= c->sub_refresh;
     const bool fresh_coarse = !c->reuse_precond || c->coarse_age < 0 || c->coarse_age >= c->coarse_refresh;
+    c->prev_sub_age = c->sub_age;
+    c->prev_coarse_age = c->coarse_age;
+    c->prev_solve_fresh = c->last_solve_fresh;
     c->sub_age = fresh_sub ? 1 : c->sub_age + 1;
     c->coarse_age = fresh_coarse ? 1 : c->coarse_age + 1;
     c->last_solve_fresh = fresh_sub && fresh_coarse;
@@ -1300,6 +1308,10 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     if (c->opt.record_passes) c->passes.push_back({e.total, r.si, revert ? 1 : 0});
     if (c->opt.record_passes >= 3) trace_eval(c, e, revert);
     if (revert) {  // solver.hpp:244-248 (x_mm of the previous pass is untouched)
+        // the device skipped this pass's solve and preconditioner rebuilds
+        c->sub_age = c->prev_sub_age;
+        c->coarse_age = c->prev_coarse_age;
+        c->last_solve_fresh = c->prev_solve_fresh;
         NRR_CUDA_CHECK(cudaMemcpyAsync(c->x.p, c->xmm.p, sizeof(double) * D, cudaMemcpyDeviceToDevice, c->stream));
         deform_run(c, c->x.p, c->vhat.p, nullptr, nullptr);
         r.current_is_aa = false;
