@@ -15,10 +15,13 @@ struct Surface {
     std::vector<std::array<int, 3>> faces;
     std::vector<std::pair<int, int>> edges;
     double avg_edge_length = 0.0;
+    /// per vertex: (neighbour, edge length), sorted (surface.hpp:24)
+    std::vector<std::vector<std::pair<int, double>>> adjacency;
 
     int point_count() const { return static_cast<int>(points.size()); }
 
-    /// surface.hpp:29-45 (mean edge length; adjacency is rebuilt where needed)
+    /// surface.hpp:29-45: mean edge length (C ABI, which also range-checks the
+    /// edges) and the sorted adjacency lists
     void finalize_edges() {
         const auto f = detail::flat(points);
         std::vector<int32_t> e(2 * edges.size());
@@ -28,6 +31,13 @@ struct Surface {
         }
         detail::check(nrr_avg_edge_length(f.data(), point_count(), e.data(), static_cast<int32_t>(edges.size()),
                                           &avg_edge_length));
+        adjacency.assign(points.size(), {});
+        for (const auto& [a, b] : edges) {
+            const double len = (points[a] - points[b]).norm();
+            adjacency[a].emplace_back(b, len);
+            adjacency[b].emplace_back(a, len);
+        }
+        for (auto& nb : adjacency) std::sort(nb.begin(), nb.end());
     }
 };
 

@@ -84,6 +84,24 @@ def build_library(force=False, verbose=False):
     return LIB
 
 
+CLI_SRC = os.path.join(PKG, "cli", "nrr_cli.cpp")
+CLI = os.path.join(PKG, "nrr")
+
+
+def build_cli(force=False):
+    """The `nrr` command-line front end (register / metrics / graph-dump) over
+    the drop-in headers and libnrr_b200.so (rpath $ORIGIN)."""
+    hdrs = [os.path.join(INCLUDE, "nrr", f) for f in os.listdir(os.path.join(INCLUDE, "nrr"))]
+    if not force and not _stale(CLI, [CLI_SRC, LIB] + hdrs):
+        return CLI
+    cmd = ["g++", "-O2", "-std=c++20", "-Wall", "-I", INCLUDE, "-o", CLI, CLI_SRC, "-L", PKG, "-lnrr_b200",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("cli build failed: %s\n%s" % (" ".join(cmd), r.stderr[-4000:]))
+    return CLI
+
+
 def build_oracle(force=False):
     """The checker (test infrastructure): oracle/_build/liboracle.so."""
     args = ["make", "-C", os.path.join(ROOT, "oracle")]
@@ -101,6 +119,7 @@ def main():
     ap.add_argument("--verbose", action="store_true")
     a = ap.parse_args()
     print(build_library(a.force, a.verbose))
+    print(build_cli(a.force))
     print(build_oracle(a.force))
 
 
