@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -189,6 +190,19 @@ public:
 private:
     nrr_ctx* ctx_ = nullptr;
 };
+
+// Setup entry points (knn_edges, build_graph) run on the B200 when one is
+// visible (bitwise equal to the host build) and on the host
+// otherwise; NRR_SETUP_HOST=1 forces the host build.
+inline bool setup_on_device() {
+    static const bool on = [] {
+        const char* e = std::getenv("NRR_SETUP_HOST");
+        if (e && *e == '1') return false;
+        int32_t c = 0;
+        return nrr_device_count(&c) == NRR_OK && c > 0;
+    }();
+    return on;
+}
 
 // per-thread device context for the stateless free functions (the reference
 // functions are pure; the device path keeps one context per host thread)

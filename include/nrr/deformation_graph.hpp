@@ -60,7 +60,8 @@ struct DeformationGraph {  // deformation_graph.hpp:50-67
     int edge_count() const { return static_cast<int>(graph_edges.size()); }
 };
 
-/// deformation_graph.hpp:157-210 (host; same sweep, geodesics and weights)
+/// deformation_graph.hpp:157-210: on the B200 when one is visible (setup_graph.cu,
+/// bitwise equal to the host sweep), else the host build
 inline DeformationGraph build_graph(const Surface& source, double radius) {
     const auto pts = detail::flat(source.points);
     std::vector<int32_t> e(2 * source.edges.size());
@@ -69,8 +70,12 @@ inline DeformationGraph build_graph(const Surface& source, double radius) {
         e[2 * i + 1] = source.edges[i].second;
     }
     nrr_graph* h = nullptr;
-    detail::check(nrr_build_graph(pts.data(), source.point_count(), e.data(),
-                                  static_cast<int32_t>(source.edges.size()), radius, &h));
+    if (detail::setup_on_device() && source.point_count() > 0)
+        detail::check(nrr_build_graph_gpu(0, pts.data(), source.point_count(), e.data(),
+                                          static_cast<int32_t>(source.edges.size()), radius, &h, nullptr));
+    else
+        detail::check(nrr_build_graph(pts.data(), source.point_count(), e.data(),
+                                      static_cast<int32_t>(source.edges.size()), radius, &h));
     int32_t N, E, S, P;
     nrr_graph_counts(h, &N, &E, &S, &P);
     const int n = source.point_count();

@@ -54,12 +54,17 @@ inline std::vector<std::pair<int, int>> edges_from_faces(const std::vector<std::
     return e;
 }
 
-inline std::vector<std::pair<int, int>> knn_edges(const std::vector<Vec3>& points, int k) {  // surface.hpp:70-94
+/// surface.hpp:70-94 (device build when a B200 is visible, k <= 32)
+inline std::vector<std::pair<int, int>> knn_edges(const std::vector<Vec3>& points, int k) {
     const auto f = detail::flat(points);
     std::vector<int32_t> out(2 * points.size() * std::max(k, 1) + 2);
     int32_t cnt = 0;
-    detail::check(nrr_knn_edges(f.data(), static_cast<int32_t>(points.size()), k, out.data(),
-                                static_cast<int32_t>(out.size() / 2), &cnt));
+    if (detail::setup_on_device() && k >= 1 && k <= 32)
+        detail::check(nrr_knn_edges_gpu(0, f.data(), static_cast<int32_t>(points.size()), k, out.data(),
+                                        static_cast<int32_t>(out.size() / 2), &cnt));
+    else
+        detail::check(nrr_knn_edges(f.data(), static_cast<int32_t>(points.size()), k, out.data(),
+                                    static_cast<int32_t>(out.size() / 2), &cnt));
     std::vector<std::pair<int, int>> e(cnt);
     for (int i = 0; i < cnt; ++i) e[i] = {out[2 * i], out[2 * i + 1]};
     return e;

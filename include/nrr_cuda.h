@@ -252,6 +252,10 @@ int nrr_edges_from_faces(const int32_t* faces, int32_t nf, int32_t n, int32_t* o
 /* knn_edges (surface.hpp:70-94), exact with (distance, index) order */
 int nrr_knn_edges(const double* pts, int32_t n, int32_t k, int32_t* out_edges, int32_t cap,
                   int32_t* out_count);
+/* limited_geodesic (geodesic.hpp:22-84): vertices with edge-graph distance
+   < radius from `source`, ascending index; out arrays may be NULL (count only) */
+int nrr_limited_geodesic(const double* pts, int32_t n, const int32_t* edges, int32_t ne, int32_t source,
+                         double radius, int32_t* out_idx, double* out_dist, int32_t cap, int32_t* out_count);
 /* Surface::finalize_edges mean edge length (surface.hpp:29-45) */
 int nrr_avg_edge_length(const double* pts, int32_t n, const int32_t* edges, int32_t ne,
                         double* out);
@@ -261,6 +265,15 @@ int nrr_normalize_pair(double* src, int32_t n, double* tgt, int32_t m, double* o
 typedef struct nrr_graph nrr_graph;
 int nrr_build_graph(const double* pts, int32_t n, const int32_t* edges, int32_t ne,
                     double radius, nrr_graph** out);
+/* ---- device setup: the same results as nrr_knn_edges /
+   nrr_build_graph, bit for bit, computed on the B200 `device` ---- */
+int nrr_device_count(int32_t* count);
+/* knn_edges on the device; k <= 32 */
+int nrr_knn_edges_gpu(int32_t device, const double* pts, int32_t n, int32_t k, int32_t* out_edges,
+                      int32_t cap, int32_t* out_count);
+/* build_graph on the device; out_rounds (may be NULL) = rounds of the node sweep */
+int nrr_build_graph_gpu(int32_t device, const double* pts, int32_t n, const int32_t* edges, int32_t ne,
+                        double radius, nrr_graph** out, int32_t* out_rounds);
 void nrr_graph_counts(const nrr_graph* g, int32_t* N, int32_t* E, int32_t* sumk, int32_t* P);
 void nrr_graph_export(const nrr_graph* g, int32_t* node_indices, double* node_positions,
                       int32_t* edges, int32_t* infl_offsets, int32_t* infl_nodes,

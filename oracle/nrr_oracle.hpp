@@ -131,7 +131,7 @@ struct Normalization {
     double scale = 1.0;
     Vec3 center;
     Vec3 apply(const Vec3& v) const { return (v - center) * scale; }
-    Vec3 invert(const Vec3& v) const { return v * (1.0 / scale) + center; }
+    Vec3 invert(const Vec3& v) const { return v / scale + center; }  // surface.hpp:118
 };
 inline Normalization normalize_pair(Surface& source, Surface& target) {
     if (source.points.empty() || target.points.empty())

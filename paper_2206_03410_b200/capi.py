@@ -133,6 +133,12 @@ _SIGS = {
     "nrr_avg_edge_length": (C.c_int, [f64p, C.c_int32, i32p, C.c_int32, f64p]),
     "nrr_normalize_pair": (C.c_int, [f64p, C.c_int32, f64p, C.c_int32, f64p]),
     "nrr_build_graph": (C.c_int, [f64p, C.c_int32, i32p, C.c_int32, C.c_double, C.POINTER(C.c_void_p)]),
+    "nrr_build_graph_gpu": (C.c_int, [C.c_int32, f64p, C.c_int32, i32p, C.c_int32, C.c_double, C.POINTER(C.c_void_p),
+                                      i32p]),
+    "nrr_knn_edges_gpu": (C.c_int, [C.c_int32, f64p, C.c_int32, C.c_int32, i32p, C.c_int32, i32p]),
+    "nrr_device_count": (C.c_int, [i32p]),
+    "nrr_limited_geodesic": (C.c_int, [f64p, C.c_int32, i32p, C.c_int32, C.c_int32, C.c_double, i32p, f64p,
+                                       C.c_int32, i32p]),
     "nrr_graph_counts": (None, [C.c_void_p, i32p, i32p, i32p, i32p]),
     "nrr_graph_export": (None, [C.c_void_p, i32p, f64p, i32p, i32p, i32p, f64p, f64p, i32p, f64p]),
     "nrr_graph_free": (None, [C.c_void_p]),

@@ -1,5 +1,7 @@
-// C ABI of the setup side (surface.hpp, deformation_graph.hpp, synthetic
-// configs); implementations in setup.cpp. CPU only, no device calls.
+// C ABI of the setup side (surface.hpp, deformation_graph.hpp, geodesic.hpp,
+// synthetic configs): host implementations in setup.cpp, the device builds
+// of kNN connectivity and the deformation graph in
+// setup_graph.cu.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -10,6 +12,9 @@
 #include "nrr_cuda.h"
 
 #include "setup.hpp"
+#include "setup_graph.hpp"
+
+#include <cuda_runtime.h>
 
 using namespace nrr_b200;
 
@@ -82,6 +87,51 @@ int nrr_build_graph(const double* pts, int32_t n, const int32_t* edges, int32_t 
             throw;
         }
         *out = h;
+    });
+}
+
+int nrr_device_count(int32_t* count) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *count = c;
+    return NRR_OK;
+}
+
+int nrr_knn_edges_gpu(int32_t device, const double* pts, int32_t n, int32_t k, int32_t* out_edges, int32_t cap,
+                      int32_t* out_count) {
+    return guarded([&] { put_edges(knn_edges_gpu(device, pts, n, k), out_edges, cap, out_count); });
+}
+
+int nrr_build_graph_gpu(int32_t device, const double* pts, int32_t n, const int32_t* edges, int32_t ne,
+                        double radius, nrr_graph** out, int32_t* out_rounds) {
+    return guarded([&] {
+        auto* h = new nrr_graph;
+        try {
+            GraphBuildStats st;
+            h->g = build_graph_gpu(device, pts, n, edges, ne, radius, &st);
+            if (out_rounds) *out_rounds = st.rounds;
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int nrr_limited_geodesic(const double* pts, int32_t n, const int32_t* edges, int32_t ne, int32_t source,
+                         double radius, int32_t* out_idx, double* out_dist, int32_t cap, int32_t* out_count) {
+    return guarded([&] {
+        const auto ball = limited_geodesic_impl(pts, n, edges, ne, source, radius);
+        *out_count = static_cast<int32_t>(ball.size());
+        if (!out_idx && !out_dist) return;
+        if (static_cast<int>(ball.size()) > cap) throw ConfigError("geodesic buffer too small");
+        for (size_t t = 0; t < ball.size(); ++t) {
+            if (out_idx) out_idx[t] = ball[t].first;
+            if (out_dist) out_dist[t] = ball[t].second;
+        }
     });
 }
 

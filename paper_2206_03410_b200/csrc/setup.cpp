@@ -292,8 +292,11 @@ P3 dominant_axis(const double cov_in[9]) {
     return {v[0 * 3 + best], v[1 * 3 + best], v[2 * 3 + best]};
 }
 
-std::vector<int> pca_order(const double* pts, int n) {
-    if (n == 0) throw ConfigError("pca_order: empty point set");
+}  // namespace
+
+// pca_order's moments (deformation_graph.hpp:79-89): mean, then the
+// covariance, both summed sequentially in point order
+void pca_moments(const double* pts, int n, double cov[9]) {
     P3 mean{0, 0, 0};
     for (int i = 0; i < n; ++i) {
         mean.x += pts[3 * i];
@@ -302,13 +305,21 @@ std::vector<int> pca_order(const double* pts, int n) {
     }
     const double inv = 1.0 / static_cast<double>(n);
     mean = {mean.x * inv, mean.y * inv, mean.z * inv};
-    double cov[9] = {0};
+    for (int k = 0; k < 9; ++k) cov[k] = 0.0;
     for (int i = 0; i < n; ++i) {
         const P3 d = sub(at3(pts, i), mean);
         const double dd[3] = {d.x, d.y, d.z};
         for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c) cov[r * 3 + c] += dd[r] * dd[c];
     }
+}
+
+namespace {
+
+std::vector<int> pca_order(const double* pts, int n) {
+    if (n == 0) throw ConfigError("pca_order: empty point set");
+    double cov[9];
+    pca_moments(pts, n, cov);
     P3 axis = dominant_axis(cov);
     if (!std::isfinite(axis.x) || !std::isfinite(axis.y) || !std::isfinite(axis.z)) axis = {1, 0, 0};
     const double comp[3] = {axis.x, axis.y, axis.z};
@@ -329,6 +340,35 @@ std::vector<int> pca_order(const double* pts, int n) {
 }
 
 }  // namespace
+
+// limited_geodesic (geodesic.hpp:22-84) over the adjacency of (pts, edges)
+std::vector<std::pair<int, double>> limited_geodesic_impl(const double* pts, int n, const int32_t* edges, int ne,
+                                                          int source, double radius) {
+    if (source < 0 || source >= n) throw ConfigError("limited_geodesic: source index out of range");
+    if (!(radius > 0.0)) throw ConfigError("limited_geodesic: radius must be positive");
+    const Adjacency adj = finalize(pts, n, edges, ne);
+    Geodesic geo(pts, n, adj);
+    std::vector<std::pair<int, double>> out;
+    geo.query(source, radius, out);
+    return out;
+}
+
+// pca_order's axis (deformation_graph.hpp:86-95) from an accumulated
+// covariance: the dominant eigenvector, (1,0,0) if not finite, sign fixed so
+// the first nonzero component is positive (used by the device build)
+void pca_axis(const double cov[9], double out[3]) {
+    P3 axis = dominant_axis(cov);
+    if (!std::isfinite(axis.x) || !std::isfinite(axis.y) || !std::isfinite(axis.z)) axis = {1, 0, 0};
+    const double comp[3] = {axis.x, axis.y, axis.z};
+    for (int c = 0; c < 3; ++c)
+        if (comp[c] != 0.0) {
+            if (comp[c] < 0.0) axis = {-axis.x, -axis.y, -axis.z};
+            break;
+        }
+    out[0] = axis.x;
+    out[1] = axis.y;
+    out[2] = axis.z;
+}
 
 GraphData build_graph_impl(const double* pts, int n, const int32_t* sedges, int ne, double radius) {
     if (n == 0) throw ConfigError("build_graph: empty source surface");

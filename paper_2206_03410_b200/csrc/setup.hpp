@@ -18,6 +18,10 @@ struct GraphData {
     std::vector<double> pair_w;
 };
 
+std::vector<std::pair<int, double>> limited_geodesic_impl(const double* pts, int n, const int32_t* edges, int ne,
+                                                          int source, double radius);
+void pca_moments(const double* pts, int n, double cov[9]);
+void pca_axis(const double cov[9], double out_axis[3]);
 GraphData build_graph_impl(const double* pts, int n, const int32_t* sedges, int ne, double radius);
 void synth_config(int which, uint64_t seed, double scale, std::vector<double>& src, std::vector<int32_t>& faces,
                   std::vector<double>& tgt);

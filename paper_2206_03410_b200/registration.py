@@ -7,6 +7,7 @@ Arrays are numpy, float64 AoS (n, 3) for points; NodeTransforms X is the
 reference's 4N x 3 column-major stacking flattened to 12N (solver.hpp:146).
 """
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 from typing import Optional
@@ -117,13 +118,45 @@ def edges_from_faces(faces, n):
     return out[: cnt.value].copy()
 
 
-def knn_edges(points, k=6):
+def _setup_device(device):
+    """Where a setup entry runs: None = the B200 when one is visible (the
+    C++ headers' rule, NRR_SETUP_HOST=1 forces the host), False = host, an
+    int = that device."""
+    if device is None:
+        if os.environ.get("NRR_SETUP_HOST") == "1":
+            return None
+        cnt = C.c_int32()
+        capi.load().nrr_device_count(C.byref(cnt))
+        return 0 if cnt.value > 0 else None
+    if device is False:
+        return None
+    return int(device)
+
+
+def knn_edges(points, k=6, device=False):
+    """knn_edges (surface.hpp:70-94); device: see _setup_device."""
     lib = capi.load()
     p = f64(points).reshape(-1, 3)
     cnt = C.c_int32()
     out = np.zeros((len(p) * k, 2), np.int32)
-    check(lib.nrr_knn_edges(d(p), len(p), k, i(out), len(out), C.byref(cnt)))
+    dev = _setup_device(device)
+    if dev is not None:
+        check(lib.nrr_knn_edges_gpu(dev, d(p), len(p), k, i(out), len(out), C.byref(cnt)))
+    else:
+        check(lib.nrr_knn_edges(d(p), len(p), k, i(out), len(out), C.byref(cnt)))
     return out[: cnt.value].copy()
+
+
+def limited_geodesic(points, edges, source, radius):
+    """limited_geodesic (geodesic.hpp:22-84): (vertex ids, distances)."""
+    lib = capi.load()
+    p, e = f64(points).reshape(-1, 3), i32(edges).reshape(-1, 2)
+    cnt = C.c_int32()
+    check(lib.nrr_limited_geodesic(d(p), len(p), i(e), len(e), source, float(radius), None, None, 0, C.byref(cnt)))
+    idx, dist = np.zeros(cnt.value, np.int32), np.zeros(cnt.value)
+    check(lib.nrr_limited_geodesic(d(p), len(p), i(e), len(e), source, float(radius), i(idx), d(dist), len(idx),
+                                   C.byref(cnt)))
+    return idx, dist
 
 
 def avg_edge_length(points, edges):
@@ -143,12 +176,20 @@ def normalize_pair(source, target):
     return s, t, out[0], out[1:4].copy()
 
 
-def build_graph(points, edges, radius):
-    """build_graph (deformation_graph.hpp:157-210)."""
+def build_graph(points, edges, radius, device=False, stats=None):
+    """build_graph (deformation_graph.hpp:157-210); device: see _setup_device.
+    `stats` (dict) receives the device sweep's round count."""
     lib = capi.load()
     p, e = f64(points).reshape(-1, 3), i32(edges).reshape(-1, 2)
     h = C.c_void_p()
-    check(lib.nrr_build_graph(d(p), len(p), i(e), len(e), float(radius), C.byref(h)))
+    dev = _setup_device(device)
+    if dev is not None:
+        rounds = C.c_int32()
+        check(lib.nrr_build_graph_gpu(dev, d(p), len(p), i(e), len(e), float(radius), C.byref(h), C.byref(rounds)))
+        if stats is not None:
+            stats["rounds"] = rounds.value
+    else:
+        check(lib.nrr_build_graph(d(p), len(p), i(e), len(e), float(radius), C.byref(h)))
     try:
         N, E, S, P = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
         lib.nrr_graph_counts(h, C.byref(N), C.byref(E), C.byref(S), C.byref(P))
