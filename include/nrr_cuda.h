@@ -157,6 +157,15 @@ int nrr_register(nrr_ctx* ctx, const nrr_problem_view* p, const nrr_solver_confi
  * all ranks) and the rank's slice of the deformed points. */
 int nrr_comm_unique_id(void* out128);
 int nrr_ctx_set_comm(nrr_ctx* ctx, const void* id128, int32_t nranks, int32_t rank);
+/* In-process group of contexts (one process, one host thread per context):
+ * the sharded path's collectives rendezvous on the host and reduce in rank
+ * order on the device. Lets the product's vertex-sharded path run with
+ * several ranks on one GPU (tests); NCCL (nrr_ctx_set_comm) is the multi-GPU
+ * path. The group must outlive its contexts' runs. */
+typedef struct nrr_local_group nrr_local_group;
+int nrr_local_group_create(int32_t nranks, nrr_local_group** out);
+void nrr_local_group_destroy(nrr_local_group* group);
+int nrr_ctx_set_local_comm(nrr_ctx* ctx, nrr_local_group* group, int32_t rank);
 int nrr_ctx_set_shard(nrr_ctx* ctx, int32_t n_global);
 
 /* report of the last run */

@@ -120,6 +120,9 @@ _SIGS = {
     "nrr_comm_unique_id": (C.c_int, [C.c_void_p]),
     "nrr_ctx_set_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
     "nrr_ctx_set_shard": (C.c_int, [C.c_void_p, C.c_int32]),
+    "nrr_local_group_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "nrr_local_group_destroy": (None, [C.c_void_p]),
+    "nrr_ctx_set_local_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "nrr_assemble": (C.c_int, [C.c_void_p, f64p, f64p, f64p, f64p, C.c_double, C.c_double,
                                C.POINTER(SolverConfig), f64p, f64p]),
     "nrr_solve": (C.c_int, [C.c_void_p, f64p, f64p, f64p, f64p]),

@@ -178,7 +178,7 @@ struct nrr_ctx {
     cudaStream_t stream = nullptr;
     // vertex sharding (comm.hpp): this rank's problem view is its vertex
     // slice; n_global = all ranks' vertices (term weights, median)
-    ncclComm_t comm = nullptr;
+    std::unique_ptr<nrr_b200::Collective> comm;  // NCCL or an in-process group (comm.hpp)
     int nranks = 1, rank = 0, n_global = -1;
     cudaStream_t side = nullptr;  // subdomain inverses run beside the coarse setup
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -301,7 +301,6 @@ struct nrr_ctx {
                 if (x) cudaEventDestroy(x);
         for (auto& x : pass_ev)
             if (x) cudaEventDestroy(x);
-        if (comm) nrr_b200::nccl().comm_destroy(comm);
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
         if (eval_done) cudaEventDestroy(eval_done);
@@ -856,7 +855,7 @@ int n_total(const nrr_ctx* c) { return c->n_global >= 0 ? c->n_global : c->n; }
 
 void allreduce(nrr_ctx* c, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op) {
     if (!c->comm) return;
-    nccl_check(nccl().all_reduce(buf, buf, count, t, op, c->comm, c->stream), "allreduce");
+    c->comm->allreduce(buf, count, t, op, c->stream);
 }
 
 // after the terms: the node terms (reg, rot) exist on rank 0 only, then the
@@ -906,7 +905,7 @@ Params init_parameters(nrr_ctx* c, const nrr_solver_config& cfg) {  // solver.hp
         NRR_CUDA_CHECK(cudaMemcpyAsync(pad.p, hpad.data(), sizeof(double) * hpad.size(), cudaMemcpyHostToDevice, c->stream));
         NRR_CUDA_CHECK(cudaMemcpyAsync(pad.p, c->d2.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
         all.resize(static_cast<size_t>(std::max(mx, 1)) * c->nranks);
-        nccl_check(nccl().all_gather(pad.p, all.p, std::max(mx, 1), ncclFloat64, c->comm, c->stream), "allgather");
+        c->comm->allgather(pad.p, all.p, std::max(mx, 1), ncclFloat64, c->stream);
         std::vector<double> h(all.n);
         NRR_CUDA_CHECK(cudaMemcpyAsync(h.data(), all.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
         sync(c);
@@ -1531,15 +1530,43 @@ int nrr_ctx_set_comm(nrr_ctx* ctx, const void* id128, int32_t nranks, int32_t ra
     return guarded([&] {
         NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
         if (nranks < 1 || rank < 0 || rank >= nranks) throw ConfigError("set_comm: bad rank / size");
-        if (ctx->comm) {
-            nccl().comm_destroy(ctx->comm);
-            ctx->comm = nullptr;
-        }
+        ctx->comm.reset();
         ctx->nranks = nranks;
         ctx->rank = rank;
         ncclUniqueId id;
         std::memcpy(&id, id128, sizeof(id));
-        nccl_check(nccl().comm_init_rank(&ctx->comm, nranks, id, rank), "comm init");
+        ctx->comm = make_nccl_collective(id, nranks, rank);
+    });
+}
+
+struct nrr_local_group {
+    std::shared_ptr<nrr_b200::LocalGroup> g;
+    int n = 0;
+};
+
+int nrr_local_group_create(int32_t nranks, nrr_local_group** out) {
+    return guarded([&] {
+        auto* h = new nrr_local_group;
+        try {
+            h->g = make_local_group(nranks);
+            h->n = nranks;
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+void nrr_local_group_destroy(nrr_local_group* g) { delete g; }
+
+int nrr_ctx_set_local_comm(nrr_ctx* ctx, nrr_local_group* group, int32_t rank) {
+    return guarded([&] {
+        if (!group || rank < 0 || rank >= group->n) throw ConfigError("set_local_comm: bad rank / group");
+        ctx->comm.reset();
+        ctx->nranks = group->n;
+        ctx->rank = rank;
+        ctx->comm = make_local_collective(group->g, rank);
     });
 }
 

@@ -133,7 +133,7 @@ def _setup_device(device):
     return int(device)
 
 
-def knn_edges(points, k=6, device=False):
+def knn_edges(points, k=6, device=None):
     """knn_edges (surface.hpp:70-94); device: see _setup_device."""
     lib = capi.load()
     p = f64(points).reshape(-1, 3)
@@ -176,7 +176,7 @@ def normalize_pair(source, target):
     return s, t, out[0], out[1:4].copy()
 
 
-def build_graph(points, edges, radius, device=False, stats=None):
+def build_graph(points, edges, radius, device=None, stats=None):
     """build_graph (deformation_graph.hpp:157-210); device: see _setup_device.
     `stats` (dict) receives the device sweep's round count."""
     lib = capi.load()
@@ -241,6 +241,23 @@ def comm_unique_id() -> bytes:
     buf = (C.c_char * 128)()
     check(lib.nrr_comm_unique_id(buf))
     return bytes(buf)
+
+
+class LocalGroup:
+    """In-process group of `world` contexts for the vertex-sharded path
+    (nrr_local_group_*): each member context is driven by its own host
+    thread; the collectives rendezvous on the host (tests on one GPU)."""
+
+    def __init__(self, world: int):
+        self.lib = capi.load()
+        self.h = C.c_void_p()
+        check(self.lib.nrr_local_group_create(world, C.byref(self.h)))
+        self.world = world
+
+    def close(self):
+        if self.h:
+            self.lib.nrr_local_group_destroy(self.h)
+            self.h = C.c_void_p()
 
 
 def make_problem(config, seed=None, scale=1.0, mult=None):
@@ -308,6 +325,10 @@ class Context:
         """Join the vertex-sharded run (NCCL communicator of this context)."""
         buf = (C.c_char * 128).from_buffer_copy(unique_id)
         check(self.lib.nrr_ctx_set_comm(self.h, buf, world, rank))
+
+    def set_local_comm(self, group: "LocalGroup", rank: int):
+        """Join an in-process group as `rank` (the sharded path on one GPU)."""
+        check(self.lib.nrr_ctx_set_local_comm(self.h, group.h, rank))
 
     def set_shard(self, n_global: int):
         """This context's problem view is one vertex slice of n_global vertices."""
