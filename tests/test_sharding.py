@@ -203,17 +203,22 @@ def test_multi_rank_sharded_path_matches_unsharded(world):
 
 @pytest.mark.gpu
 def test_multi_rank_sharded_headline_step():
-    """Config 2 (99,856 vertices) split over 4 in-process ranks: 10 fixed-count
-    AA iterations, energies equal the unsharded run to 1e-9 relative."""
+    """Config 2 (99,856 vertices) split over 4 in-process ranks, 10 fixed-count
+    iterations. Plain MM: energies equal the unsharded run to 1e-9 relative
+    (only the allreduce's summation order differs). With Anderson the same
+    ulp-level differences grow ~10x per accelerated iteration (the trajectory
+    chaos of DESIGN.md §4), so the AA run is held to the north_star's 1e-6."""
     p = R.make_problem(2)
     ref = R.Context()
     ref.set_problem(p)
     prm = ref.init_parameters()
-    kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300, i_max=10)
-    _, _, r0 = ref.register(R.solver_config(**kw), one_shot_problem=p)
+    for aa, tol in ((0, 1e-9), (5, 1e-6)):
+        kw = dict(nu_a_init=prm["nu_a"], nu_a_min=prm["nu_a"], nu_r_init=prm["nu_r"], eps=1e-300, i_max=10,
+                  aa_window=aa)
+        _, _, r0 = ref.register(R.solver_config(**kw), one_shot_problem=p)
+        res = _sharded_run(p, 4, kw)
+        e_ref = np.array([it["E"] for st in r0["stages"] for it in st["iterations"]])
+        e = np.array([it["E"] for st in res[0][2]["stages"] for it in st["iterations"]])
+        assert len(e) == len(e_ref) == 10
+        assert np.all(np.abs(e - e_ref) <= tol * np.abs(e_ref)), (aa, np.max(np.abs(e - e_ref) / np.abs(e_ref)))
     ref.close()
-    res = _sharded_run(p, 4, kw)
-    e_ref = np.array([it["E"] for st in r0["stages"] for it in st["iterations"]])
-    e = np.array([it["E"] for st in res[0][2]["stages"] for it in st["iterations"]])
-    assert len(e) == len(e_ref) == 10
-    assert np.all(np.abs(e - e_ref) <= 1e-9 * np.abs(e_ref))
