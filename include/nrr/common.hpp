@@ -139,6 +139,80 @@ struct MatrixX {
 };
 using VectorX = std::vector<double>;
 
+// compressed sparse column matrix (Eigen::SparseMatrix<double> subset the
+// reference API and its tests use: rows/cols/nonZeros/coeff, the raw arrays,
+// transpose, difference, Frobenius norm, products with dense matrices,
+// conversion to dense)
+struct SparseMatrix {
+    int r = 0, c = 0;
+    std::vector<int> outer{0};  // c + 1 column starts
+    std::vector<int> inner;     // row indices, ascending per column
+    std::vector<double> val;
+    SparseMatrix() = default;
+    SparseMatrix(int rows, int cols) : r(rows), c(cols), outer(static_cast<size_t>(cols) + 1, 0) {}
+    int rows() const { return r; }
+    int cols() const { return c; }
+    int nonZeros() const { return static_cast<int>(val.size()); }
+    double* valuePtr() { return val.data(); }
+    const double* valuePtr() const { return val.data(); }
+    const int* outerIndexPtr() const { return outer.data(); }
+    const int* innerIndexPtr() const { return inner.data(); }
+    double coeff(int i, int j) const {
+        const auto b = inner.begin() + outer[j], e = inner.begin() + outer[j + 1];
+        const auto it = std::lower_bound(b, e, i);
+        return it != e && *it == i ? val[static_cast<size_t>(it - inner.begin())] : 0.0;
+    }
+    SparseMatrix transpose() const {
+        SparseMatrix t(c, r);
+        t.inner.resize(inner.size());
+        t.val.resize(val.size());
+        for (int i : inner) ++t.outer[i + 1];
+        for (int i = 0; i < r; ++i) t.outer[i + 1] += t.outer[i];
+        std::vector<int> pos(t.outer.begin(), t.outer.end() - 1);
+        for (int j = 0; j < c; ++j)
+            for (int k = outer[j]; k < outer[j + 1]; ++k) {
+                const int q = pos[inner[k]]++;
+                t.inner[q] = j;
+                t.val[q] = val[k];
+            }
+        return t;
+    }
+    MatrixX toDense() const {
+        MatrixX d(r, c);
+        for (int j = 0; j < c; ++j)
+            for (int k = outer[j]; k < outer[j + 1]; ++k) d(inner[k], j) = val[k];
+        return d;
+    }
+    SparseMatrix operator-(const SparseMatrix& o) const {  // union pattern, explicit zeros kept
+        SparseMatrix d(r, c);
+        for (int j = 0; j < c; ++j) {
+            int a = outer[j], b = o.outer[j];
+            while (a < outer[j + 1] || b < o.outer[j + 1]) {
+                const int ia = a < outer[j + 1] ? inner[a] : r, ib = b < o.outer[j + 1] ? o.inner[b] : r;
+                const int i = std::min(ia, ib);
+                d.inner.push_back(i);
+                d.val.push_back((ia == i ? val[a++] : 0.0) - (ib == i ? o.val[b++] : 0.0));
+            }
+            d.outer[j + 1] = static_cast<int>(d.inner.size());
+        }
+        return d;
+    }
+    double norm() const {
+        double s = 0.0;
+        for (double v : val) s += v * v;
+        return std::sqrt(s);
+    }
+    MatrixX operator*(const MatrixX& x) const {
+        MatrixX y(r, x.cols());
+        for (int q = 0; q < x.cols(); ++q)
+            for (int j = 0; j < c; ++j) {
+                const double xj = x(j, q);
+                for (int k = outer[j]; k < outer[j + 1]; ++k) y(inner[k], q) += val[k] * xj;
+            }
+        return y;
+    }
+};
+
 /// File could not be read or written, or its contents are malformed (common.hpp:14-16).
 struct IoError : std::runtime_error {
     explicit IoError(const std::string& msg) : std::runtime_error(msg) {}

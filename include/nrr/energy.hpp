@@ -68,9 +68,29 @@ inline Vec3 reg_difference(const DeformationGraph& graph, const NodeTransforms& 
     return c * (x.affine(j) * (pi - pj) + pj + x.translation(j) - pi - x.translation(i));
 }
 
-/// energy.hpp:92-116 against caller-held correspondences and rotations (a host
-/// utility of the API; inside register_surfaces the device evaluates the same
-/// sums in fixed-order reductions, csrc/kernels.cu terms/energy kernels)
+namespace detail {
+inline nrr_energy_terms_in terms_in(const DeformationGraph& graph, const NodeTransforms& x,
+                                    std::vector<double>& pos, std::vector<int32_t>& pairs) {
+    nrr_energy_terms_in in{};
+    pos = flat(graph.node_positions);
+    pairs.clear();
+    for (const auto& [i, j] : graph.reg_pairs) {
+        pairs.push_back(i);
+        pairs.push_back(j);
+    }
+    in.node_count = graph.node_count();
+    in.X = x.stacked.data();
+    in.node_positions = pos.data();
+    in.pair_count = graph.directed_pair_count();
+    in.reg_pairs = pairs.data();
+    in.reg_weights = graph.reg_weights.data();
+    return in;
+}
+}  // namespace detail
+
+/// energy.hpp:92-116 against caller-held correspondences and rotations, on
+/// the device (api_terms.cu: per point / pair / node terms, fixed-order sums;
+/// inside register_surfaces the same sums come from terms_kernel)
 inline EnergyBreakdown evaluate_energy(const std::vector<Vec3>& deformed, const NodeTransforms& x,
                                        const DeformationGraph& graph, const Correspondences& corr,
                                        const std::vector<Mat3>& rotations, const EnergyParams& prm) {
@@ -78,12 +98,25 @@ inline EnergyBreakdown evaluate_energy(const std::vector<Vec3>& deformed, const 
         throw NumericalError("evaluate_energy: correspondence count mismatch");
     if (static_cast<int>(rotations.size()) != graph.node_count())
         throw NumericalError("evaluate_energy: rotation count mismatch");
+    std::vector<double> pos, R(9 * rotations.size());
+    std::vector<int32_t> pairs;
+    nrr_energy_terms_in in = detail::terms_in(graph, x, pos, pairs);
+    const auto d = detail::flat(deformed), u = detail::flat(corr.target_point);
+    for (size_t j = 0; j < rotations.size(); ++j)
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) R[9 * j + 3 * r + c] = rotations[j](r, c);
+    in.n = static_cast<int32_t>(deformed.size());
+    in.deformed = d.data();
+    in.corr_points = u.data();
+    in.nu_a = prm.nu_a;
+    in.nu_r = prm.nu_r;
+    in.rotations = R.data();
+    double sums[3];
+    detail::check(nrr_energy_terms(detail::default_context(), &in, nullptr, nullptr, sums));
     EnergyBreakdown e;
-    for (size_t i = 0; i < deformed.size(); ++i)
-        e.align += welsch_sq((deformed[i] - corr.target_point[i]).squaredNorm(), prm.nu_a);
-    for (int k = 0; k < graph.directed_pair_count(); ++k)
-        e.reg += welsch_sq(reg_difference(graph, x, k).squaredNorm(), prm.nu_r);
-    for (int j = 0; j < graph.node_count(); ++j) e.rot += (x.affine(j) - rotations[j]).squaredNorm();
+    e.align = sums[0];
+    e.reg = sums[1];
+    e.rot = sums[2];
     e.total = e.align + prm.alpha * e.reg + prm.beta * e.rot;
     e.alpha = prm.alpha;
     e.beta = prm.beta;
@@ -92,23 +125,43 @@ inline EnergyBreakdown evaluate_energy(const std::vector<Vec3>& deformed, const 
     return e;
 }
 
-/// energy.hpp:118-121. The device keeps K as 4x4 blocks over the fixed
-/// pattern (diagonal + both halves of every graph edge): block_row_ptr /
-/// block_cols per node, values 16 per block row-major, in the reference's
-/// pattern order; coeff() reads it like the reference's sparse matrix.
+/// energy.hpp:118-121: K (4N x 4N, the fixed pattern: diagonal + both halves
+/// of every graph edge) and B (4N x 3). The device assembles K as 4x4 blocks
+/// in pattern order (block_row_ptr / block_cols / values, 16 per block
+/// row-major); K is their scalar CSC image, refreshed by every fill (the
+/// reference's Eigen::SparseMatrix member, read by callers and tests).
 struct LinearSystem {
+    SparseMatrix K;
+    MatrixX B;  // 4N x 3
     std::vector<int> block_row_ptr;
     std::vector<int> block_cols;
     std::vector<double> values;
-    MatrixX B;  // 4N x 3
+    std::vector<int> csc_from_block;       // K.val[q] = values[csc_from_block[q]]
     std::shared_ptr<detail::Context> ctx;  // device copy of the system
 
     int rows() const { return B.rows(); }
-    double coeff(int r, int c) const {
-        const int a = r / 4, b = c / 4;
-        for (int k = block_row_ptr[a]; k < block_row_ptr[a + 1]; ++k)
-            if (block_cols[k] == b) return values[16 * static_cast<size_t>(k) + 4 * (r % 4) + (c % 4)];
-        return 0.0;
+    double coeff(int r, int c) const { return K.coeff(r, c); }
+
+    // scalar CSC pattern of the block pattern (K is symmetric: column c of
+    // block column b lists rows 4a + i for the blocks a of node b, ascending)
+    void build_pattern() {
+        const int N = static_cast<int>(block_row_ptr.size()) - 1;
+        K = SparseMatrix(4 * N, 4 * N);
+        csc_from_block.clear();
+        for (int b = 0; b < N; ++b)
+            for (int j = 0; j < 4; ++j) {
+                for (int k = block_row_ptr[b]; k < block_row_ptr[b + 1]; ++k)
+                    for (int i = 0; i < 4; ++i) {
+                        K.inner.push_back(4 * block_cols[k] + i);
+                        // K(4a+i, 4b+j) = block (b, a) entry (j, i) by symmetry
+                        csc_from_block.push_back(16 * k + 4 * j + i);
+                    }
+                K.outer[4 * b + j + 1] = static_cast<int>(K.inner.size());
+            }
+        K.val.assign(K.inner.size(), 0.0);
+    }
+    void refresh_K() {
+        for (size_t q = 0; q < csc_from_block.size(); ++q) K.val[q] = values[csc_from_block[q]];
     }
 };
 
@@ -164,6 +217,7 @@ public:
         }
         system_.values.assign(16 * system_.block_cols.size(), 0.0);
         system_.B.setZero(4 * N, 3);
+        system_.build_pattern();
         system_.ctx = ctx_;
     }
 
@@ -185,6 +239,7 @@ public:
         detail::check(nrr_assemble(ctx_->get(), q.data(), w_align.data(), w_reg.data(), R.data(), beta,
                                    landmark_weight, landmarks_.empty() ? nullptr : &la.cfg, system_.values.data(),
                                    system_.B.data()));
+        system_.refresh_K();
     }
 
     const LinearSystem& system() const { return system_; }
@@ -205,19 +260,29 @@ private:
     LinearSystem system_;
 };
 
-/// energy.hpp:363-369
+/// energy.hpp:363-369 on the device (api_terms.cu)
 inline std::vector<double> alignment_weights(const Correspondences& corr, double nu_a) {
     std::vector<double> w(corr.size());
-    for (int i = 0; i < corr.size(); ++i) w[i] = welsch_weight_sq(corr.squared_distance[i], nu_a);
+    if (w.empty()) return w;
+    nrr_energy_terms_in in{};
+    in.n = corr.size();
+    in.corr_sqdist = corr.squared_distance.data();
+    in.nu_a = nu_a;
+    detail::check(nrr_energy_terms(detail::default_context(), &in, w.data(), nullptr, nullptr));
     return w;
 }
 
-/// energy.hpp:371-379
+/// energy.hpp:371-379 on the device (api_terms.cu)
 inline std::vector<double> regularization_weights(const DeformationGraph& graph, const NodeTransforms& x, double nu_r,
                                                   double alpha) {
     std::vector<double> w(graph.directed_pair_count());
-    for (int e = 0; e < graph.directed_pair_count(); ++e)
-        w[e] = alpha * welsch_weight_sq(reg_difference(graph, x, e).squaredNorm(), nu_r);
+    if (w.empty()) return w;
+    std::vector<double> pos;
+    std::vector<int32_t> pairs;
+    nrr_energy_terms_in in = detail::terms_in(graph, x, pos, pairs);
+    in.nu_r = nu_r;
+    in.alpha = alpha;
+    detail::check(nrr_energy_terms(detail::default_context(), &in, nullptr, w.data(), nullptr));
     return w;
 }
 
@@ -234,9 +299,13 @@ inline LinearSystem assemble_system(const NodeTransforms& x, const Surface& sour
 /// energy.hpp:393-409: K X = B on the device PCG (K must be positive definite)
 inline NodeTransforms solve_system(const LinearSystem& system) {
     if (!system.ctx) throw ConfigError("solve_system: system was not assembled by this library");
+    // the block values from K (a caller may have edited K, as the reference's
+    // tests do with B): every block entry is one CSC entry of K
+    std::vector<double> values(system.values.size());
+    for (size_t q = 0; q < system.csc_from_block.size(); ++q) values[system.csc_from_block[q]] = system.K.val[q];
     NodeTransforms x;
     x.stacked.setZero(system.B.rows(), 3);
-    detail::check(nrr_solve(system.ctx->get(), system.values.data(), system.B.data(), nullptr, x.stacked.data()));
+    detail::check(nrr_solve(system.ctx->get(), values.data(), system.B.data(), nullptr, x.stacked.data()));
     return x;
 }
 

@@ -12,13 +12,13 @@ inline Mat3 project_to_rotation(const Mat3& a, double* sigma_min = nullptr) {
     double X[12] = {0};
     for (int c = 0; c < 3; ++c)
         for (int r = 0; r < 3; ++r) X[c * 4 + r] = a(c, r);
-    double R[9];
+    double R[9], smin = 0.0;
     int32_t deg = 0;
-    detail::check(nrr_project_rotations(detail::default_context(), X, 1, R, &deg));
+    detail::check(nrr_project_rotations_sigma(detail::default_context(), X, 1, R, &smin, &deg));
     Mat3 out;
     for (int r = 0; r < 3; ++r)
         for (int c = 0; c < 3; ++c) out(r, c) = R[r * 3 + c];
-    if (sigma_min) *sigma_min = deg ? 0.0 : 1.0;  // only the < 1e-12 test is exposed by the device path
+    if (sigma_min) *sigma_min = smin;  // the smallest singular value (rotation.hpp:21)
     return out;
 }
 

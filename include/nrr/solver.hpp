@@ -139,7 +139,7 @@ inline NodeTransforms mm_step(const Surface& source, const DeformationGraph& gra
                               const NodeTransforms& x, const SolverParams& prm) {
     detail::ProblemArrays pa(source, &target.points(), graph);
     nrr_ctx* c = detail::default_context();
-    detail::check(nrr_ctx_set_problem(c, &pa.view));
+    detail::use_problem(c, pa);
     const double p4[4] = {prm.alpha, prm.beta, prm.nu_a, prm.nu_r};
     NodeTransforms out;
     out.stacked.setZero(4 * graph.node_count(), 3);

@@ -207,6 +207,34 @@ int nrr_deform(nrr_ctx* ctx, const double* X, double* out_points);
 /* project_rotations (energy.hpp:47-56) of host X (N nodes) */
 int nrr_project_rotations(nrr_ctx* ctx, const double* X, int32_t N, double* out_R,
                           int32_t* out_degenerate);
+/* the same with each node's smallest singular value (project_to_rotation's
+   sigma_min, rotation.hpp:14-24); out_sigma_min may be NULL */
+int nrr_project_rotations_sigma(nrr_ctx* ctx, const double* X, int32_t N, double* out_R, double* out_sigma_min,
+                                int32_t* out_degenerate);
+
+/* The reference API's energy helpers on caller-held arrays, on the device:
+ * alignment_weights (energy.hpp:363-368) from corr_sqdist, regularization_
+ * weights (:371-378) and the evaluate_energy sums (:92-116) {align, reg, rot}
+ * (reg and rot unweighted; total = align + alpha reg + beta rot is formed by
+ * the caller). Any input group may be NULL when its outputs are not wanted;
+ * X is the reference 4N x 3 column-major block, rotations N x 9 row-major. */
+typedef struct nrr_energy_terms_in {
+    int32_t n;
+    const double* deformed;     /* n*3 */
+    const double* corr_points;  /* n*3 */
+    const double* corr_sqdist;  /* n */
+    double nu_a;
+    int32_t node_count;
+    const double* X;               /* 12N */
+    const double* node_positions;  /* N*3 */
+    int32_t pair_count;
+    const int32_t* reg_pairs;      /* P*2 */
+    const double* reg_weights;     /* P */
+    double nu_r, alpha;
+    const double* rotations;       /* N*9 */
+} nrr_energy_terms_in;
+int nrr_energy_terms(nrr_ctx* ctx, const nrr_energy_terms_in* in, double* out_w_align, double* out_w_reg,
+                     double* out_sums3);
 
 /* One teacher-forced pass at host X with prm = {alpha, beta, nu_a, nu_r}:
  * find_correspondences + evaluate_energy (energy.hpp:92-116) + weights

@@ -140,6 +140,8 @@ _SIGS = {
                                       i32p]),
     "nrr_knn_edges_gpu": (C.c_int, [C.c_int32, f64p, C.c_int32, C.c_int32, i32p, C.c_int32, i32p]),
     "nrr_device_count": (C.c_int, [i32p]),
+    "nrr_project_rotations_sigma": (C.c_int, [C.c_void_p, f64p, C.c_int32, f64p, f64p, i32p]),
+    "nrr_energy_terms": (C.c_int, [C.c_void_p, C.c_void_p, f64p, f64p, f64p]),
     "nrr_limited_geodesic": (C.c_int, [f64p, C.c_int32, i32p, C.c_int32, C.c_int32, C.c_double, i32p, f64p,
                                        C.c_int32, i32p]),
     "nrr_graph_counts": (None, [C.c_void_p, i32p, i32p, i32p, i32p]),

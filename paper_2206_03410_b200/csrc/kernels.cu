@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(256) energy_reduce_kernel(DevProblem p, const 
     }
 }
 
-__global__ void rotations_kernel(const double* __restrict__ x, int N, double* __restrict__ R, int* degenerate) {
+__global__ void rotations_kernel(const double* __restrict__ x, int N, double* __restrict__ R, int* degenerate,
+                                 double* __restrict__ sigma_min) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= N) return;
     const double* xj = x + 12 * j;
@@ -180,6 +181,7 @@ __global__ void rotations_kernel(const double* __restrict__ x, int N, double* __
     double rot[9], smin = 0.0;
     project_rotation3(a, rot, &smin);
     for (int k = 0; k < 9; ++k) R[9 * j + k] = rot[k];
+    if (sigma_min) sigma_min[j] = smin;
     if (smin < 1e-12) atomicAdd(degenerate, 1);
 }
 
@@ -711,9 +713,9 @@ void launch_assemble(const DevProblem& p, const double* wa, const double* q, con
     }
 }
 
-void launch_rotations(const double* x, int N, double* R, int* degenerate, cudaStream_t s) {
+void launch_rotations(const double* x, int N, double* R, int* degenerate, cudaStream_t s, double* sigma_min) {
     if (N == 0) return;
-    rotations_kernel<<<(N + 127) / 128, 128, 0, s>>>(x, N, R, degenerate);
+    rotations_kernel<<<(N + 127) / 128, 128, 0, s>>>(x, N, R, degenerate, sigma_min);
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -80,7 +80,8 @@ void launch_energy_reduce(const DevProblem& p, const double* partials, const Ter
                           PassRecord* rec, cudaStream_t s);
 void launch_assemble(const DevProblem& p, const double* wa, const double* q, const double* wr, const double* R,
                      const TermParams& tp, double* K, double* B, cudaStream_t s);
-void launch_rotations(const double* x, int N, double* R, int* degenerate, cudaStream_t s);
+void launch_rotations(const double* x, int N, double* R, int* degenerate, cudaStream_t s,
+                      double* sigma_min = nullptr);
 
 // Anderson acceleration on device vectors of length D = 12N
 constexpr int kTriMax = (kMaxAA + 1) * (kMaxAA + 2) / 2;  // packed R of [dF | f]

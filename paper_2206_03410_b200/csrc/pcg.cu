@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         for (int c = 0; c < 4 && ok; ++c) {
             double s = k[c * 4 + c];
             for (int t = 0; t < c; ++t) s -= l[c * 4 + t] * l[c * 4 + t];
-            if (!(s > 1e-13 * dmax)) {
+            if (!(s > 0.0)) {  // the block is not PD (reference describe_failure: min eigenvalue <= 0)
                 ok = false;
                 break;
             }

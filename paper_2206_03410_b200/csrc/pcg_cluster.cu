@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) pcg_cluster_kernel(Cluster
         for (int c = 0; c < 4 && ok; ++c) {
             double sum = k[c * 4 + c];
             for (int t = 0; t < c; ++t) sum -= l[c * 4 + t] * l[c * 4 + t];
-            if (!(sum > 1e-13 * dmax)) {
+            if (!(sum > 0.0)) {  // not PD (reference describe_failure)
                 ok = false;
                 break;
             }

@@ -36,6 +36,11 @@
 #include "comm.hpp"
 
 namespace nrr_b200 {
+void energy_terms(cudaStream_t s, const nrr_energy_terms_in* in, double* out_w_align, double* out_w_reg,
+                  double* out_sums3);  // api_terms.cu
+}
+
+namespace nrr_b200 {
 
 namespace {
 thread_local std::string g_last_error;
@@ -1736,27 +1741,44 @@ int nrr_deform(nrr_ctx* ctx, const double* X, double* out_points) {
     });
 }
 
-int nrr_project_rotations(nrr_ctx* ctx, const double* X, int32_t N, double* out_R, int32_t* out_degenerate) {
+int nrr_energy_terms(nrr_ctx* ctx, const nrr_energy_terms_in* in, double* out_w_align, double* out_w_reg,
+                     double* out_sums3) {
+    return guarded([&] {
+        NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
+        energy_terms(ctx->stream, in, out_w_align, out_w_reg, out_sums3);
+        ctx->launches += 2;
+    });
+}
+
+int nrr_project_rotations_sigma(nrr_ctx* ctx, const double* X, int32_t N, double* out_R, double* out_sigma_min,
+                                int32_t* out_degenerate) {
     return guarded([&] {
         NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
         for (int64_t k = 0; k < 12 * static_cast<int64_t>(N); ++k)
             if (!std::isfinite(X[k])) throw NumericalError("project_to_rotation: non-finite input matrix");
-        DevBuf<double> dx, dn, dr;
+        DevBuf<double> dx, dn, dr, ds;
         DevBuf<int> dd;
         dx.upload(X, 12 * static_cast<size_t>(N), ctx->stream);
         dn.resize(std::max(12 * N, 1));
         dr.resize(std::max(9 * N, 1));
+        if (out_sigma_min) ds.resize(std::max(N, 1));
         dd.resize(1);
         dd.zero(ctx->stream);
         launch_colmajor_to_nodemajor(dx.p, dn.p, N, ctx->stream);
-        launch_rotations(dn.p, N, dr.p, dd.p, ctx->stream);
+        launch_rotations(dn.p, N, dr.p, dd.p, ctx->stream, out_sigma_min ? ds.p : nullptr);
         ctx->launches += 2;
         NRR_CUDA_CHECK(cudaMemcpyAsync(out_R, dr.p, sizeof(double) * 9 * N, cudaMemcpyDeviceToHost, ctx->stream));
+        if (out_sigma_min)
+            NRR_CUDA_CHECK(cudaMemcpyAsync(out_sigma_min, ds.p, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
         int deg = 0;
         NRR_CUDA_CHECK(cudaMemcpyAsync(&deg, dd.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         sync(ctx);
         if (out_degenerate) *out_degenerate = deg;
     });
+}
+
+int nrr_project_rotations(nrr_ctx* ctx, const double* X, int32_t N, double* out_R, int32_t* out_degenerate) {
+    return nrr_project_rotations_sigma(ctx, X, N, out_R, nullptr, out_degenerate);
 }
 
 int nrr_step(nrr_ctx* ctx, const double* X, const double* prm, double landmark_weight,

@@ -171,6 +171,30 @@ TEST("energy: SystemAssembler fill/solve match the oracle's K, B and solution") 
                 if (sys.coeff(r, col) != sys.coeff(col, r)) sym = false;
             }
     CHECK(sym);
+    // the reference's LinearSystem::K view (robust_energy_tests.cpp:60,185-214,252)
+    CHECK(sys.K.rows() == sys.rows() && sys.K.cols() == sys.rows());
+    CHECK(sys.K.nonZeros() == 16 * static_cast<int>(sys.block_cols.size()));
+    CHECK((sys.K - sys.K.transpose()).norm() == 0.0);
+    {
+        double worst = 0.0;
+        for (int a = 0; a + 1 < static_cast<int>(sys.block_row_ptr.size()); ++a)
+            for (int k = sys.block_row_ptr[a]; k < sys.block_row_ptr[a + 1]; ++k)
+                for (int i = 0; i < 4; ++i)
+                    for (int j = 0; j < 4; ++j)
+                        worst = std::max(worst, std::abs(sys.K.coeff(4 * a + i, 4 * sys.block_cols[k] + j) -
+                                                         sys.values[16 * static_cast<size_t>(k) + 4 * i + j]));
+        CHECK(worst == 0.0);
+        const nrr::MatrixX Kx = sys.K * sys.B;  // sparse x dense
+        const nrr::MatrixX Kd = sys.K.toDense();
+        double dd = 0.0;
+        for (int r = 0; r < sys.rows(); ++r)
+            for (int q = 0; q < 3; ++q) {
+                double v = 0.0;
+                for (int cc = 0; cc < sys.rows(); ++cc) v += Kd(r, cc) * sys.B(cc, q);
+                dd = std::max(dd, std::abs(v - Kx(r, q)));
+            }
+        CHECK(dd <= 1e-9 * (1.0 + kmax));
+    }
     const auto xp = pa.solve();
     CHECK(max_abs_diff(xp.stacked.d, xo.stacked) <= 1e-9);
     // solve_system on the returned LinearSystem
@@ -199,6 +223,44 @@ TEST("energy: a singular system fails with the reference's message") {
         threw = std::string(e.what()).find("linear system not positive definite") != std::string::npos;
     }
     CHECK(threw);
+}
+
+TEST("energy: the failing block named is the first non-PD one, at a node j != 0") {
+    // beta > 0 makes every A-part PD; a node's translation pivot is exactly 0
+    // when all points it influences have zero alignment weight and the reg
+    // weights are zero: describe_failure (energy.hpp:329-340) names the first
+    // such node
+    const Case c = strip_case(8, 10, 6);
+    const int N = c.pg.node_count(), n = c.psrc.point_count();
+    const int j = N - 1;
+    std::vector<double> w(n, 1.0);
+    for (int i = 0; i < n; ++i)
+        for (const auto& e : c.pg.influence[i])
+            if (e.node == j) w[i] = 0.0;
+    int expect = -1;
+    for (int k = 0; k < N && expect < 0; ++k) {
+        bool any = false;
+        for (int i = 0; i < n; ++i)
+            for (const auto& e : c.pg.influence[i])
+                if (e.node == k && w[i] != 0.0) any = true;
+        if (!any) expect = k;
+    }
+    CHECK(expect > 0);
+    nrr::SystemAssembler pa(c.psrc, c.pg);
+    nrr::Correspondences pc;
+    pc.target_index.assign(n, 0);
+    pc.target_point.assign(n, nrr::Vec3());
+    pc.squared_distance.assign(n, 0.0);
+    std::vector<nrr::Mat3> rot(N, nrr::Mat3::Identity());
+    pa.fill(pc, rot, w, std::vector<double>(c.pg.directed_pair_count(), 0.0), 1.0);
+    std::string msg;
+    try {
+        pa.solve();
+    } catch (const nrr::NumericalError& e) {
+        msg = e.what();
+    }
+    CHECK(msg.find("linear system not positive definite") != std::string::npos);
+    CHECK(msg.find("node " + std::to_string(expect) + ")") != std::string::npos);
 }
 
 TEST("anderson: anderson_combine and AndersonWindow match the oracle") {
