@@ -524,6 +524,14 @@ def run_pairs(args, dist):
     dev_ms = e0.elapsed_time(e1)
     iters = sum(counts)
     launches = sum(c.stats()["launches"] for c, _ in ctxs) - launches0
+    # algorithmic bytes of the timed iterations (SURVEY 8(d) per pair, with
+    # each pair's own PCG iteration count)
+    step_bytes = 0.0
+    for (ctx, _), p in zip(ctxs, probs):
+        g = p.graph
+        step_bytes += (args.pair_iters * iteration_fixed_bytes(p.n, len(p.target), len(g.infl_nodes), g.node_count,
+                                                               g.pair_count)
+                       + ctx.stats()["pcg_iterations"] * pcg_bytes_per_iteration(g.node_count, g.pair_count))
     for ctx, _ in ctxs:
         ctx.finish()
         ctx.close()
@@ -552,6 +560,17 @@ def run_pairs(args, dist):
     max_ms = dist.max(dev_ms)
     total = dist.sum(float(iters))
     e2e = dist.sum(float(sum(e2e_counts))) / dist.max(wall)
+    all_bytes = dist.sum(step_bytes)
+    peak, peak_src = load_peaks()
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        host = host_cpu()
+        threads = host["nproc"] or 1
+        cv, cpairs, csec = reference_pairs(args, threads)
+        cpu = {"value": cv, "unit": UNIT, "cores": threads, "kind": "port", "host": host,
+               "pairs_per_s": cpairs / csec,
+               "sample": f"{cpairs} pairs x {args.pair_iters} fixed-count iterations of the oracle restatement on "
+                         f"{threads} threads (one registration per thread, the reference's model)"}
     if dist.rank == 0:
         g = probs[0].graph
         line = {
@@ -566,6 +585,11 @@ def run_pairs(args, dist):
                        "l2": "not flushed: the batch (all pairs resident) exceeds L2, each pair's working set "
                              "stays resident during its own iterations",
                        "pairs_per_s": args.pairs / (max_ms / 1e3)},
+            "roofline": {"bound": "hbm", "kernel": "whole step (all kernels of every pair)",
+                         "achieved": all_bytes / (max_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": all_bytes / (max_ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                         "bytes_per_step": all_bytes / max(1.0, total)},
+            "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": UNIT, "seconds": wall, "note": "wall clock, fresh contexts, incl. per-pair setup"},
             "gpu_launches": launches, "clocks": clocks.result(),
         }
