@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
                 sn[sp + rank] = (cl << 27) | c;
                 sd[sp + rank] = bd;
             }
+            if (sp + cnt > kStack && lane == 0 && bv.overflow) atomicOr(bv.overflow, 1);  // the host raises
             sp = min(sp + cnt, kStack);
             __syncwarp(gmask);
         }

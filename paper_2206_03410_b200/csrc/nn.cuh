@@ -34,6 +34,7 @@ struct BvhView {
     double cx, cy, cz;
     float half_extent;
     unsigned long long* stats;  // optional (NRR_NN_STATS): [internal visits, leaf visits, leaf hits, queries]
+    int* overflow;              // set when a traversal stack overflowed (children would be dropped: the host raises)
     // uniform grid over the same points (warm-started queries whose search
     // ball covers few cells skip the tree): cells of size h from (glx, gly,
     // glz) relative to the centre, cell-major float4 points, cell_start[ncells+1]

@@ -220,6 +220,7 @@ struct nrr_ctx {
     DevBuf<double4> d_infl_f, d_pair_gv, d_cfa, d_cfb;
     DevBuf<double> d_med_sorted;
     DevBuf<unsigned long long> nn_stats;
+    DevBuf<int> nn_overflow;  // BVH traversal-stack overflow flag (nn.cu)
     DevBuf<unsigned char> d_med_tmp;
     DevBuf<int> d_edge_of_blk, d_setup_flags, d_skip;
     const int* pcg_skip = nullptr;  // device skip flag for the next solve (speculative pass)
@@ -368,6 +369,14 @@ void nn_run(nrr_ctx* c, const double* queries, int nq, const int* prev, int* idx
     c->nn_ready = false;
 }
 
+void check_nn_overflow(nrr_ctx* c) {
+    if (!c->nn_overflow.p) return;
+    int ov = 0;
+    NRR_CUDA_CHECK(cudaMemcpyAsync(&ov, c->nn_overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    NRR_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    if (ov) throw CudaError("nearest-neighbour traversal stack overflow (the result would be inexact)");
+}
+
 void set_target(nrr_ctx* c, const double* tgt, int m, bool built = false) {
     if (m <= 0) throw NumericalError("SpatialIndex: cannot index an empty point set");
     if (!built) c->bvh.build(tgt, m);
@@ -418,6 +427,9 @@ void set_target(nrr_ctx* c, const double* tgt, int m, bool built = false) {
             b.gmax_cells = gc ? std::atoi(gc) : 216;
         }
     }
+    c->nn_overflow.resize(1);
+    c->nn_overflow.zero(c->stream);
+    b.overflow = c->nn_overflow.p;
     b.stats = nullptr;
     if (std::getenv("NRR_NN_STATS")) {
         c->nn_stats.resize(4);
@@ -1421,6 +1433,7 @@ void run_finish(nrr_ctx* c, double* out_X, double* out_deformed) {
     c->eval_queued = false;
     if (!r.active) throw ConfigError("no registration in progress (nrr_ctx_begin)");
     if (r.stage_open) close_stage(c);  // stopped early: record the partial stage
+    check_nn_overflow(c);
     const auto t2 = std::chrono::steady_clock::now();
     const int N = c->N, n = c->n;
     if (out_X) {
@@ -1716,6 +1729,7 @@ int nrr_nearest_from(nrr_ctx* ctx, const double* queries, int32_t q, const int32
         NRR_CUDA_CHECK(cudaMemcpyAsync(out_index, di.p, sizeof(int) * q, cudaMemcpyDeviceToHost, ctx->stream));
         NRR_CUDA_CHECK(cudaMemcpyAsync(d2.data(), dd.p, sizeof(double) * q, cudaMemcpyDeviceToHost, ctx->stream));
         sync(ctx);
+        check_nn_overflow(ctx);
         for (int i = 0; i < q; ++i) out_distance[i] = std::sqrt(d2[i]);  // kd_tree.hpp:128
     });
 }
