@@ -480,4 +480,224 @@ void build_grid(const double* tgt64, int m, const double center[3], const double
     NRR_CUDA_CHECK(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- device BVH build
+// The same index as BvhHost::build (Morton order by a stable radix sort of the
+// 30-bit codes, float4 points relative to the centre, 8-point leaves, 8-ary
+// FP32 box levels), built on the device: identical bits, no host pass over
+// the targets beyond the box reduction's few partials.
+namespace {
+constexpr int kBvhBlocks = 296;
+__device__ __forceinline__ unsigned spread10_bvh(unsigned v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void bvh_bbox_kernel(const double* __restrict__ t, int m, double* __restrict__ part, int* __restrict__ bad) {
+    __shared__ double sh[6][256];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    bool nf = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        for (int c = 0; c < 3; ++c) {
+            const double v = t[3 * i + c];
+            nf |= !isfinite(v);
+            lo[c] = fmin(lo[c], v);
+            hi[c] = fmax(hi[c], v);
+        }
+    if (nf) atomicOr(bad, 1);
+    for (int c = 0; c < 3; ++c) {
+        sh[c][threadIdx.x] = lo[c];
+        sh[3 + c][threadIdx.x] = hi[c];
+    }
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int c = 0; c < 3; ++c) {
+                sh[c][threadIdx.x] = fmin(sh[c][threadIdx.x], sh[c][threadIdx.x + o]);
+                sh[3 + c][threadIdx.x] = fmax(sh[3 + c][threadIdx.x], sh[3 + c][threadIdx.x + o]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) part[6 * blockIdx.x + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// Morton code (BvhHost::build's arithmetic) and max |t - centre| partials
+__global__ void bvh_code_kernel(const double* __restrict__ t, int m, double l0, double l1, double l2, double ext,
+                                double c0, double c1, double c2, unsigned* __restrict__ code, int* __restrict__ idx,
+                                double* __restrict__ hpart) {
+    __shared__ double sh[256];
+    double h = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const double v[3] = {t[3 * i], t[3 * i + 1], t[3 * i + 2]};
+        const double lo[3] = {l0, l1, l2}, ct[3] = {c0, c1, c2};
+        unsigned k = 0;
+        for (int c = 0; c < 3; ++c) {
+            const double u = ext > 0 ? (v[c] - lo[c]) / ext : 0.0;
+            const unsigned q = static_cast<unsigned>(fmin(1023.0, fmax(0.0, u * 1024.0)));
+            k |= spread10_bvh(q) << c;
+            h = fmax(h, fabs(v[c] - ct[c]));
+        }
+        code[i] = k;
+        idx[i] = i;
+    }
+    sh[threadIdx.x] = h;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) hpart[blockIdx.x] = sh[0];
+}
+
+__global__ void bvh_points_kernel(const double* __restrict__ t, int m, int mpad, const int* __restrict__ order,
+                                  double c0, double c1, double c2, float4* __restrict__ pts) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= mpad) return;
+    float4 p = make_float4(1e18f, 1e18f, 1e18f, 0.f);
+    int idx = -1;
+    if (k < m) {
+        idx = order[k];
+        p.x = static_cast<float>(t[3 * idx] - c0);
+        p.y = static_cast<float>(t[3 * idx + 1] - c1);
+        p.z = static_cast<float>(t[3 * idx + 2] - c2);
+    }
+    memcpy(&p.w, &idx, 4);
+    pts[k] = p;
+}
+
+// level 0: one box per 8 points (valid points only); level l: per 8 children
+__global__ void bvh_leaf_box_kernel(const float4* __restrict__ pts, int m, int cnt, float4* __restrict__ lo,
+                                    float4* __restrict__ hi) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    float4 l = make_float4(INFINITY, INFINITY, INFINITY, 0), h = make_float4(-INFINITY, -INFINITY, -INFINITY, 0);
+    for (int t = 0; t < 8; ++t) {
+        const int p = 8 * k + t;
+        if (p >= m) break;
+        const float4 q = pts[p];
+        l.x = fminf(l.x, q.x);
+        l.y = fminf(l.y, q.y);
+        l.z = fminf(l.z, q.z);
+        h.x = fmaxf(h.x, q.x);
+        h.y = fmaxf(h.y, q.y);
+        h.z = fmaxf(h.z, q.z);
+    }
+    lo[k] = l;
+    hi[k] = h;
+}
+__global__ void bvh_level_box_kernel(float4* __restrict__ lo, float4* __restrict__ hi, int prev_off, int prev_cnt,
+                                     int off, int cnt) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    float4 l = make_float4(INFINITY, INFINITY, INFINITY, 0), h = make_float4(-INFINITY, -INFINITY, -INFINITY, 0);
+    for (int t = 0; t < 8; ++t) {
+        const int c = 8 * k + t;
+        if (c >= prev_cnt) break;
+        const float4 cl = lo[prev_off + c], ch = hi[prev_off + c];
+        l.x = fminf(l.x, cl.x);
+        l.y = fminf(l.y, cl.y);
+        l.z = fminf(l.z, cl.z);
+        h.x = fmaxf(h.x, ch.x);
+        h.y = fmaxf(h.y, ch.y);
+        h.z = fmaxf(h.z, ch.z);
+    }
+    lo[off + k] = l;
+    hi[off + k] = h;
+}
+}  // namespace
+
+void bvh_layout(int m, std::vector<int>& level_off, std::vector<int>& level_cnt, int& total_boxes) {
+    level_off.clear();
+    level_cnt.clear();
+    int cnt = (m + 7) / 8;
+    level_off.push_back(0);
+    level_cnt.push_back(cnt);
+    total_boxes = cnt;
+    while (cnt > 8) {
+        cnt = (cnt + 7) / 8;
+        level_off.push_back(total_boxes);
+        level_cnt.push_back(cnt);
+        total_boxes += cnt;
+    }
+    if (level_cnt.size() > static_cast<size_t>(kMaxLevels - 1))
+        throw NumericalError("SpatialIndex: target too large for the BVH level table");
+}
+
+size_t bvh_scratch_bytes(int m) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const unsigned*>(nullptr), static_cast<unsigned*>(nullptr),
+                                    static_cast<const int*>(nullptr), static_cast<int*>(nullptr), m, 0, 30);
+    return 4 * a256(sizeof(int) * static_cast<size_t>(std::max(m, 1))) + a256(b) +
+           a256(sizeof(double) * 6 * kBvhBlocks) + a256(sizeof(double) * kBvhBlocks) + 512;
+}
+
+void build_bvh_device(const double* tgt64, int m, BvhHost& meta, float4* pts, float4* box_lo, float4* box_hi,
+                      void* scratch, cudaStream_t s) {
+    if (m <= 0) throw NumericalError("SpatialIndex: cannot index an empty point set");
+    meta.m = m;
+    char* p = static_cast<char*>(scratch);
+    const size_t eb = a256(sizeof(int) * static_cast<size_t>(m));
+    unsigned* code = reinterpret_cast<unsigned*>(p);
+    unsigned* code2 = reinterpret_cast<unsigned*>(p + eb);
+    int* idx = reinterpret_cast<int*>(p + 2 * eb);
+    int* order = reinterpret_cast<int*>(p + 3 * eb);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, code, code2, idx, order, m, 0, 30);
+    void* tmp = p + 4 * eb;
+    double* part = reinterpret_cast<double*>(p + 4 * eb + a256(tb));
+    double* hpart = part + 6 * kBvhBlocks;
+    int* bad = reinterpret_cast<int*>(hpart + kBvhBlocks);
+    NRR_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    bvh_bbox_kernel<<<kBvhBlocks, 256, 0, s>>>(tgt64, m, part, bad);
+    NRR_CUDA_CHECK(cudaGetLastError());
+    std::vector<double> h(6 * kBvhBlocks + 1);
+    int hbad = 0;
+    NRR_CUDA_CHECK(cudaMemcpyAsync(h.data(), part, sizeof(double) * 6 * kBvhBlocks, cudaMemcpyDeviceToHost, s));
+    NRR_CUDA_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NRR_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (hbad) throw NumericalError("SpatialIndex: non-finite target point");
+    for (int c = 0; c < 3; ++c) {
+        meta.lo[c] = INFINITY;
+        meta.hi[c] = -INFINITY;
+    }
+    for (int b = 0; b < kBvhBlocks; ++b)
+        for (int c = 0; c < 3; ++c) {
+            meta.lo[c] = std::min(meta.lo[c], h[6 * b + c]);
+            meta.hi[c] = std::max(meta.hi[c], h[6 * b + 3 + c]);
+        }
+    double ext = 0;
+    for (int c = 0; c < 3; ++c) {
+        meta.center[c] = 0.5 * (meta.lo[c] + meta.hi[c]);
+        ext = std::max(ext, meta.hi[c] - meta.lo[c]);
+    }
+    bvh_code_kernel<<<kBvhBlocks, 256, 0, s>>>(tgt64, m, meta.lo[0], meta.lo[1], meta.lo[2], ext, meta.center[0],
+                                               meta.center[1], meta.center[2], code, idx, hpart);
+    NRR_CUDA_CHECK(cudaGetLastError());
+    NRR_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, code, code2, idx, order, m, 0, 30, s));
+    const int mpad = (m + 7) / 8 * 8;
+    bvh_points_kernel<<<(mpad + 255) / 256, 256, 0, s>>>(tgt64, m, mpad, order, meta.center[0], meta.center[1],
+                                                         meta.center[2], pts);
+    NRR_CUDA_CHECK(cudaGetLastError());
+    int total = 0;
+    bvh_layout(m, meta.level_off, meta.level_cnt, total);
+    bvh_leaf_box_kernel<<<(meta.level_cnt[0] + 255) / 256, 256, 0, s>>>(pts, m, meta.level_cnt[0], box_lo, box_hi);
+    NRR_CUDA_CHECK(cudaGetLastError());
+    for (size_t l = 1; l < meta.level_cnt.size(); ++l) {
+        bvh_level_box_kernel<<<(meta.level_cnt[l] + 255) / 256, 256, 0, s>>>(
+            box_lo, box_hi, meta.level_off[l - 1], meta.level_cnt[l - 1], meta.level_off[l], meta.level_cnt[l]);
+        NRR_CUDA_CHECK(cudaGetLastError());
+    }
+    std::vector<double> hp(kBvhBlocks);
+    NRR_CUDA_CHECK(cudaMemcpyAsync(hp.data(), hpart, sizeof(double) * kBvhBlocks, cudaMemcpyDeviceToHost, s));
+    NRR_CUDA_CHECK(cudaStreamSynchronize(s));
+    meta.half_extent = 0;
+    for (double v : hp) meta.half_extent = std::max(meta.half_extent, v);
+    meta.pts.clear();  // device-resident
+    meta.box_lo.clear();
+    meta.box_hi.clear();
+}
+
 }  // namespace nrr_b200

@@ -61,4 +61,13 @@ void build_grid(const double* tgt64, int m, const double center[3], const double
 void launch_nn(const BvhView& bv, const double* queries, int nq, const int* prev_idx, int* out_idx, double* out_d2,
                double* out_q, const double* anchor, cudaStream_t s);
 
+// The BvhHost index built on the device (bitwise the same): fills the meta
+// fields of `meta` (centre, box, half extent, level layout; its host point /
+// box vectors stay empty) and the device arrays pts (mpad), box_lo / box_hi
+// (bvh_layout's total). scratch: bvh_scratch_bytes(m).
+void bvh_layout(int m, std::vector<int>& level_off, std::vector<int>& level_cnt, int& total_boxes);
+size_t bvh_scratch_bytes(int m);
+void build_bvh_device(const double* tgt64, int m, BvhHost& meta, float4* pts, float4* box_lo, float4* box_hi,
+                      void* scratch, cudaStream_t s);
+
 }  // namespace nrr_b200

@@ -203,6 +203,7 @@ struct nrr_ctx {
     // ---- target (SpatialIndex)
     BvhHost bvh;
     DevBuf<float4> d_pts, d_lo, d_hi, d_gpts;
+    DevBuf<unsigned char> d_bvh_scratch;
     DevBuf<int> d_cell_start;
     DevBuf<unsigned char> d_grid_scratch;
     DevBuf<double> d_tgt;
@@ -377,13 +378,27 @@ void check_nn_overflow(nrr_ctx* c) {
     if (ov) throw CudaError("nearest-neighbour traversal stack overflow (the result would be inexact)");
 }
 
-void set_target(nrr_ctx* c, const double* tgt, int m, bool built = false) {
+// SpatialIndex ctor: the BVH is built on the device (nn.cu build_bvh_device,
+// the same bits as BvhHost::build); NRR_BVH_HOST=1 builds it on the host
+void set_target(nrr_ctx* c, const double* tgt, int m) {
     if (m <= 0) throw NumericalError("SpatialIndex: cannot index an empty point set");
-    if (!built) c->bvh.build(tgt, m);
     c->d_tgt.upload(tgt, static_cast<size_t>(m) * 3, c->stream);
-    c->d_pts.upload(c->bvh.pts.data(), c->bvh.pts.size(), c->stream);
-    c->d_lo.upload(c->bvh.box_lo.data(), c->bvh.box_lo.size(), c->stream);
-    c->d_hi.upload(c->bvh.box_hi.data(), c->bvh.box_hi.size(), c->stream);
+    if (std::getenv("NRR_BVH_HOST")) {
+        c->bvh.build(tgt, m);
+        c->d_pts.upload(c->bvh.pts.data(), c->bvh.pts.size(), c->stream);
+        c->d_lo.upload(c->bvh.box_lo.data(), c->bvh.box_lo.size(), c->stream);
+        c->d_hi.upload(c->bvh.box_hi.data(), c->bvh.box_hi.size(), c->stream);
+    } else {
+        std::vector<int> off, cnt;
+        int total = 0;
+        bvh_layout(m, off, cnt, total);
+        c->d_pts.resize((m + 7) / 8 * 8);
+        c->d_lo.resize(total);
+        c->d_hi.resize(total);
+        c->d_bvh_scratch.resize(bvh_scratch_bytes(m));
+        build_bvh_device(c->d_tgt.p, m, c->bvh, c->d_pts.p, c->d_lo.p, c->d_hi.p, c->d_bvh_scratch.p, c->stream);
+        c->launches += 6 + static_cast<int>(cnt.size());
+    }
     BvhView& b = c->bv;
     b.pts = c->d_pts.p;
     b.box_lo = c->d_lo.p;
@@ -1650,26 +1665,10 @@ int nrr_register(nrr_ctx* ctx, const nrr_problem_view* p, const nrr_solver_confi
         NRR_CUDA_CHECK(cudaSetDevice(ctx->device));
         validate(*cfg);
         if (p->n == 0 || p->m == 0) throw NumericalError("register_surfaces: empty surface");
-        // the target index (host BVH build) and the problem plan are
-        // independent host work: overlap them
-        std::exception_ptr bvh_err;
-        std::thread bvh([&] {
-            try {
-                ctx->bvh.build(p->target, p->m);
-            } catch (...) {
-                bvh_err = std::current_exception();
-            }
-        });
-        std::exception_ptr plan_err;
-        try {
-            set_problem(ctx, p);
-        } catch (...) {
-            plan_err = std::current_exception();
-        }
-        bvh.join();
-        if (bvh_err) std::rethrow_exception(bvh_err);
-        if (plan_err) std::rethrow_exception(plan_err);
-        set_target(ctx, p->target, p->m, true);
+        // the target index is built on the device; its kernels run while the
+        // host builds the problem plan
+        set_target(ctx, p->target, p->m);
+        set_problem(ctx, p);
         run_register(ctx, *cfg, out_X, out_deformed);
     });
 }
