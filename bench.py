@@ -443,6 +443,12 @@ def run_b200(args, dist):
             "kernel_ms_per_step": {k: v / K for k, v in kms.items()},
             "kernel_ms_note": "per-class CUDA events over K further passes (the timed passes run without them)",
             "pcg_iterations_per_step": pcg_iters / K,
+            **({"sharded_split_ms_per_step": {
+                "per_vertex (deform + nn + terms + assembly)": sum(kms[k] for k in ("deform", "nn", "terms",
+                                                                                      "assemble")) / K,
+                "allreduce (K, B)": (s1["comm_ms"] - s0["comm_ms"]) / K,
+                "replicated solve (pcg)": kms["pcg"] / K, "replicated anderson": kms["aa"] / K},
+                "nccl_ranks": dist.world} if sharded else {}),
             "nn_queries_per_s": n / (kms["nn"] / K / 1e3) if kms["nn"] > 0 else None,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -275,6 +275,9 @@ int nrr_init_parameters(nrr_ctx* ctx, const nrr_solver_config* cfg, double* out6
  * the last run: [0]=NN, [1]=terms+energy, [2]=assembly, [3]=PCG, [4]=AA,
  * [5]=deform. */
 int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* pcg_iters);
+/* CUDA-event time of the per-pass K/B allreduce of a vertex-sharded context
+   (timing on), accumulated like the kernel classes of nrr_ctx_stats */
+int nrr_ctx_comm_ms(nrr_ctx* ctx, double* out_ms);
 int nrr_ctx_enable_timing(nrr_ctx* ctx, int32_t on);
 
 /* host-only probe of the cluster-resident PCG plan for a problem (no device

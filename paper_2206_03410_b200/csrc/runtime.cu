@@ -293,7 +293,7 @@ struct nrr_ctx {
     std::vector<int> trace_nn;
 
     // ---- timing (CUDA events per kernel class)
-    static constexpr int kClasses = 6;
+    static constexpr int kClasses = 7;  // nn, terms, assembly, pcg, aa, deform, K/B allreduce
     cudaEvent_t ev[kClasses][2] = {};
     double class_ms[kClasses] = {0};
     int pcg_iters_total = 0;
@@ -327,7 +327,7 @@ struct nrr_ctx {
 namespace nrr_b200 {
 namespace {
 
-enum Cls { kNN = 0, kTerms = 1, kAsm = 2, kPcg = 3, kAA = 4, kDeform = 5 };
+enum Cls { kNN = 0, kTerms = 1, kAsm = 2, kPcg = 3, kAA = 4, kDeform = 5, kComm = 6 };
 
 struct ClassTimer {
     nrr_ctx* c;
@@ -1319,6 +1319,7 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     c->dp.skip = c->d_skip.p;
     assemble(c, tp);
     if (c->comm) {  // the replicated solve needs the full K and B (north_star: allreduce before the solve)
+        ClassTimer tc(c, kComm);
         allreduce(c, c->K.p, 16 * static_cast<size_t>(c->dp.nnzb), ncclFloat64, ncclSum);
         allreduce(c, c->B.p, 12 * static_cast<size_t>(N), ncclFloat64, ncclSum);
     }
@@ -1355,6 +1356,7 @@ bool one_pass(nrr_ctx* c, bool* stage_end) {
     nrr_iteration_record rec{e.total, e.align, e.reg, e.rot, e.landmark, 0.0, r.current_is_aa ? 1 : 0, r.si};
     std::swap(c->xmm.p, c->xmm_spec.p);
     ran[kAsm] = ran[kPcg] = true;
+    ran[kComm] = c->comm != nullptr;
     aa_push_combine(c, r.win, c->xmm.p, c->x.p, nullptr, c->xnext.p, D);
     ran[kAA] = true;
     r.current_is_aa = r.win.extrapolating();
@@ -2049,6 +2051,11 @@ int nrr_debug_solver_plan(const nrr_problem_view* p, int32_t num_sms, int64_t sm
     });
 }
 
+int nrr_ctx_comm_ms(nrr_ctx* ctx, double* out_ms) {
+    *out_ms = ctx->class_ms[kComm];
+    return 0;
+}
+
 int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* pcg_iters) {
     if (ctx->prof.n && std::getenv("NRR_PROF")) {
         long long h[32];
@@ -2083,7 +2090,7 @@ int nrr_ctx_stats(nrr_ctx* ctx, int64_t* launches, double* kernel_ms6, int32_t* 
     }
     if (launches) *launches = ctx->launches;
     if (kernel_ms6)
-        for (int k = 0; k < nrr_ctx::kClasses; ++k) kernel_ms6[k] = ctx->class_ms[k];
+        for (int k = 0; k < 6; ++k) kernel_ms6[k] = ctx->class_ms[k];
     if (pcg_iters) *pcg_iters = ctx->pcg_iters_total;
     return 0;
 }

@@ -493,8 +493,11 @@ class Context:
         ms = np.zeros(6)
         it = C.c_int32()
         self.lib.nrr_ctx_stats(self.h, C.byref(n), d(ms), C.byref(it))
+        comm = np.zeros(1)
+        self.lib.nrr_ctx_comm_ms(self.h, d(comm))
         return {"launches": n.value, "kernel_ms": {"nn": ms[0], "terms": ms[1], "assemble": ms[2], "pcg": ms[3],
-                                                    "aa": ms[4], "deform": ms[5]}, "pcg_iterations": it.value}
+                                                    "aa": ms[4], "deform": ms[5]}, "pcg_iterations": it.value,
+                "comm_ms": comm[0]}
 
 
 def bsr_pattern(graph: Graph):

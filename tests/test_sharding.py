@@ -145,6 +145,7 @@ def _sharded_run(p, world, cfg_kw, group_rank_cfg=None):
     grp = R.LocalGroup(world)
     ctxs = [R.Context() for _ in range(world)]
     out, errs = [None] * world, []
+    comm_ms = [0.0] * world
 
     def run(r):
         try:
@@ -152,7 +153,9 @@ def _sharded_run(p, world, cfg_kw, group_rank_cfg=None):
             c = ctxs[r]
             c.set_local_comm(grp, r)
             c.set_shard(p.n)
+            c.enable_timing(True)
             out[r] = c.register(R.solver_config(**cfg_kw), one_shot_problem=R.shard_problem(p, v0, v1))
+            comm_ms[r] = c.stats()["comm_ms"]
         except Exception as e:  # surfaced below
             errs.append(e)
 
@@ -166,6 +169,7 @@ def _sharded_run(p, world, cfg_kw, group_rank_cfg=None):
     grp.close()
     if errs:
         raise errs[0]
+    assert all(ms > 0 for ms in comm_ms), comm_ms  # the K/B allreduce is timed (bench's sharded split)
     return out
 
 
