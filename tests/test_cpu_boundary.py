@@ -115,3 +115,34 @@ def test_knn_edges_ties_match_exhaustive():
     pts = np.array(np.meshgrid(g, g, g, indexing="ij")).reshape(3, -1).T.copy()
     pts = pts[np.random.default_rng(1).permutation(len(pts))]
     assert np.array_equal(R.knn_edges(pts, 6), O.knn_edges(pts, 6))
+
+
+def test_limited_geodesic_matches_dijkstra():
+    """limited_geodesic (geodesic.hpp:22-84): the vertices whose edge-graph
+    distance from the source is < R, ascending, with their distances; checked
+    against scipy's Dijkstra restricted to the Euclidean ball's connected
+    component (the reference's BFS-then-Dijkstra construction)."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import dijkstra
+    from tests.helpers import make_strip
+
+    pts, faces = make_strip(20, 9)
+    pts = pts + np.random.default_rng(3).normal(0, 0.01, pts.shape)
+    e = R.edges_from_faces(faces, len(pts))
+    lbar = R.avg_edge_length(pts, e)
+    for src, mult in ((0, 3.0), (97, 4.5), (150, 2.0)):
+        radius = mult * lbar
+        idx, dist = R.limited_geodesic(pts, e, src, radius)
+        ball = np.linalg.norm(pts - pts[src], axis=1) < radius
+        w = np.linalg.norm(pts[e[:, 0]] - pts[e[:, 1]], axis=1)
+        keep = ball[e[:, 0]] & ball[e[:, 1]]
+        A = sp.coo_matrix((w[keep], (e[keep, 0], e[keep, 1])), shape=(len(pts), len(pts)))
+        d = dijkstra(A, directed=False, indices=src)
+        expect = np.nonzero(d < radius)[0]
+        assert np.array_equal(idx, expect)
+        assert np.allclose(dist, d[expect], rtol=1e-14, atol=1e-15)
+        assert idx[0] <= src <= idx[-1] and dist[np.searchsorted(idx, src)] == 0.0
+    with pytest.raises(capi.ConfigError):
+        R.limited_geodesic(pts, e, len(pts), 1.0)
+    with pytest.raises(capi.ConfigError):
+        R.limited_geodesic(pts, e, 0, -1.0)
