@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--pairs", type=int, default=256, help="config 3: number of independent pairs")
     ap.add_argument("--pair-streams", type=int, default=6, help="config 3: pairs run side by side per GPU")
     ap.add_argument("--pair-iters", type=int, default=50, help="config 3: MM iterations per pair")
+    ap.add_argument("--pair-ctas", type=int, default=0,
+                    help="config 3: PCG grid cap per pair (0 = SMs / pair-streams)")
     return ap.parse_args()
 
 
@@ -482,7 +484,7 @@ def run_pairs(args, dist):
     probs = [R.make_problem(3, seed=4000 + q) for q in mine]
     sms = torch.cuda.get_device_properties(dist.local).multi_processor_count
     S = max(1, min(args.pair_streams, len(mine)))
-    cap = max(8, sms // S)
+    cap = args.pair_ctas if args.pair_ctas > 0 else max(8, sms // S)
 
     def prepare(p):
         ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol, max_ctas=cap)
