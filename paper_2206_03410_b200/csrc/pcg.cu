@@ -1036,6 +1036,14 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         rr[k] = ur[k] = wr[k] = pr[k] = sr[k] = qr[k] = zv[k] = 0.0;
     }
 
+    // Parities of the exchanged vector Z and of the iteration partials: every
+    // publish (write before a grid barrier, read by other CTAs after it)
+    // alternates between two buffers. With one barrier per iteration a CTA
+    // that leaves the barrier early can finish the next iteration's local
+    // work and publish again while a late CTA is still reading the previous
+    // publish; with two buffers that write goes to the other parity, and the
+    // next write to this parity needs the late CTA at the next barrier first.
+    int zph = 0, pph = 0;
     // the thread's first kHaloRegs halo elements: global offsets resolved once,
     // so a fill is kHaloRegs independent L2 loads (one round trip)
     constexpr int kHaloRegs = 4;
@@ -1052,7 +1060,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         double hv[kHaloRegs];
 #pragma unroll
         for (int k = 0; k < kHaloRegs; ++k) hv[k] = hoff[k] >= 0 ? __ldcg(v + hoff[k]) : 0.0;
-        if (totals) iter_totals(a, a.part_a, G, sh.bcast, sh.ptq);
+        if (totals) iter_totals(a, a.part_a + pph * a.part_stride, G, sh.bcast, sh.ptq);
         for (int t = nrows * 12 + threadIdx.x + kHaloRegs * blockDim.x; t < n_ext * 12; t += blockDim.x)
             sh.ext[t] = __ldcg(v + static_cast<size_t>(a.ext_node[e0 + t / 12]) * 12 + t % 12);
 #pragma unroll
@@ -1158,7 +1166,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         for (int k = 0; k < EPT; ++k)
             if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = v[k];
         __syncthreads();
-        if (with_partials) partials_reduce(a.use_coarse ? 19 : 7, sh.red, a.part_a);
+        if (with_partials) partials_reduce(a.use_coarse ? 19 : 7, sh.red, a.part_a + pph * a.part_stride);
         for (int t = threadIdx.x; t < 16 * nrows; t += blockDim.x) {
             const int i = t >> 2, q = t & 3, lr = i >> 2;
             const int ch = sh.rchunk[lr], st = sh.cstart[ch];
@@ -1203,7 +1211,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         for (int k = 0; k < EPT; ++k) {
             if (el_row[k] < 0) continue;
             const double z = sh.zz[el_row[k] * 12 + my_rc];
-            __stcg(a.Z + el_g[k], z);
+            __stcg(a.Z + zph * a.z_stride + el_g[k], z);
             sh.ext[el_row[k] * 12 + my_rc] = z;
         }
     };
@@ -1312,7 +1320,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             block_partials(vals, 14, sh.red, a.part_b, 0x3u);
             precond_sub(rr, false);
             grid.sync();
-            exchange(a.Z, false);
+            exchange(a.Z + zph * a.z_stride, false);
+            zph ^= 1;
             grid_totals(a.part_b, G, sh.bcast, 2, 0x3u);
             if (a.use_coarse) aggregate_sums(a, a.part_b, G, 2, sh.ptq, 4);
             __syncthreads();
@@ -1367,7 +1376,9 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         grid.sync();
         mark(2);
         cstart_t();
-        exchange(a.Z, true);
+        exchange(a.Z + zph * a.z_stride, true);
+        zph ^= 1;
+        pph ^= 1;
         mark(3);
         const double rmax = sh.bcast[6];
         if (rmax <= tol) {  // recursive residual converged: verify on the true residual

@@ -46,14 +46,16 @@ struct PcgArgs {
     const double* K;      // nnzb*16
     const double* B;      // 12N node-major (by node id)
     double* X;            // 12N node-major: in = warm start, out = solution
-    double* Z;            // 12N scratch (preconditioned residual, exchanged)
+    double* Z;            // 2 x 12N scratch (preconditioned residual, exchanged), two parities
+    size_t z_stride;      // doubles between the parities of Z (>= 12N)
     const int* row_begin; // grid+1
     const double* node_pos;  // N*3
     const double* agg_center;  // n_agg*3
     const int* node_agg;  // N: aggregate of node
     const double* coarse_inv;  // n_c x n_c
     const double* sub_inv;     // grid x sub_chunks x (4 sub_rows x sub_ld): subdomain inverses
-    double* part_a;       // kPcgSlots x round_up(grid, 8), slot-major (iteration partials)
+    double* part_a;       // 2 parities x kPartReplicas x kPcgSlots x round_up(grid, 8), slot-major (iteration partials)
+    size_t part_stride;   // doubles between the parities of part_a
     double* part_b;       // grid*kPcgSlots
     PcgStatus* status;
     const int* skip;      // nonzero: the pass reverts, setup kernels and the solve return at once

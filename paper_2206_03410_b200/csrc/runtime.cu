@@ -741,7 +741,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     d.edge_pba = c->d_edge_pba.p;
     // state buffers
     const size_t D = 12 * static_cast<size_t>(N);
-    for (auto* b : {&c->x, &c->xmm, &c->xmm_spec, &c->xnext, &c->B, &c->Z}) b->resize(std::max<size_t>(D, 1));
+    for (auto* b : {&c->x, &c->xmm, &c->xmm_spec, &c->xnext, &c->B}) b->resize(std::max<size_t>(D, 1));
+    c->Z.resize(2 * std::max<size_t>(D, 1));  // two parities (pcg.cu: exchanged vector, see PcgArgs::z_stride)
     c->d_skip.resize(1);
     for (auto* b : {&c->vhat, &c->vhat2, &c->q}) b->resize(std::max<size_t>(3 * static_cast<size_t>(n), 1));
     c->d2.resize(std::max(n, 1));
@@ -756,7 +757,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     c->d_status.resize(1);
     clk.lap("uploads");
     if (N > 0) {
-        c->plan.size_smem(c->h_row_ptr.data(), c->h_col.data(), c->smem_optin);
+        // the kernels' static shared memory (<= 1 KB) comes out of the same opt-in budget
+        c->plan.size_smem(c->h_row_ptr.data(), c->h_col.data(), c->smem_optin - 1024);
         clk.lap("pcg smem plan");
         if (clk.on) {
             const PcgPlan& pl = c->plan;
@@ -781,7 +783,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
         c->coarse_inv.resize(nc * nc);
         c->sub_inv.resize(static_cast<size_t>(c->plan.grid) * c->plan.sub_chunks * 4 * c->plan.sub_rows *
                           c->plan.sub_ld);
-        c->pcg_a.resize(8 * kPcgSlots * static_cast<size_t>((c->plan.grid + 7) & ~7));  // kPartReplicas copies
+        // kPartReplicas copies, two parities (PcgArgs::part_stride)
+        c->pcg_a.resize(2 * 8 * kPcgSlots * static_cast<size_t>((c->plan.grid + 7) & ~7));
         c->pcg_a.zero(s);  // slot rows are padded to a multiple of 8 CTAs: the padding stays 0
         c->pcg_b.resize(kPcgSlots * static_cast<size_t>(c->plan.grid));
         d.node_row = c->d_node_row.p;
@@ -1051,6 +1054,8 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     a.B = c->B.p;
     a.X = xout;
     a.Z = c->Z.p;
+    a.z_stride = std::max<size_t>(12 * static_cast<size_t>(c->N), 1);
+    a.part_stride = 8 * kPcgSlots * static_cast<size_t>((c->plan.grid + 7) & ~7);
     a.row_begin = c->row_begin.p;
     a.node_pos = c->d_node_pos.p;
     a.agg_center = c->d_agg_center.p;
