@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--pcg-rtol", type=float, default=None, help="override the library default (1e-13)")
     ap.add_argument("--pairs", type=int, default=256, help="config 3: number of independent pairs")
-    ap.add_argument("--pair-streams", type=int, default=6, help="config 3: pairs run side by side per GPU")
+    ap.add_argument("--pair-streams", type=int, default=9,
+                    help="config 3: pairs run side by side per GPU (9: 7.5K vs 7.2K it/s at 6, profiles/r02_sweep_*)")
     ap.add_argument("--pair-iters", type=int, default=50, help="config 3: MM iterations per pair")
     ap.add_argument("--pair-ctas", type=int, default=0,
                     help="config 3: PCG grid cap per pair (0 = SMs / pair-streams)")
@@ -403,17 +404,23 @@ def run_b200(args, dist):
     ctx.close()  # the one-shot call below creates its own context, as a user would
     # end-to-end through the C ABI with host buffers (uploads, index build,
     # init_parameters, K iterations, downloads), wall clock around the call
-    e2e_ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
-    if sharded:
-        join_shard(R, e2e_ctx, dist, p_full.n)
+    # (three fresh one-shot registrations; the median is reported: a single
+    # ~40 ms wall-clock sample carries the host's scheduling noise)
     cfg_e2e = R.solver_config(i_max=K, **cfg_kw)
-    dist.barrier()
-    t0 = time.perf_counter()
-    e2e_ctx.register(cfg_e2e, one_shot_problem=p)
-    e2e_s = time.perf_counter() - t0
-    e2e_iters = e2e_ctx.report()["total_iterations"]
-    e2e_ctx.close()
-    e2e_value = (float(e2e_iters) if sharded else dist.sum(float(e2e_iters))) / dist.max(e2e_s)
+    e2e_samples = []
+    for _ in range(3):
+        e2e_ctx = R.Context(device=dist.local, pcg_rtol=args.pcg_rtol)
+        if sharded:
+            join_shard(R, e2e_ctx, dist, p_full.n)
+        dist.barrier()
+        t0 = time.perf_counter()
+        e2e_ctx.register(cfg_e2e, one_shot_problem=p)
+        e2e_s = dist.max(time.perf_counter() - t0)
+        e2e_iters = e2e_ctx.report()["total_iterations"]
+        e2e_ctx.close()
+        e2e_samples.append((float(e2e_iters) if sharded else dist.sum(float(e2e_iters))) / e2e_s)
+    e2e_value = float(np.median(e2e_samples))
+    e2e_s = float(e2e_iters) / e2e_value if sharded else K / (e2e_value / max(1, dist.world))
     h2d, d2h = h2d_d2h_bytes(p)
 
     cpu = None
@@ -454,7 +461,8 @@ def run_b200(args, dist):
             "nn_queries_per_s": n / (kms["nn"] / K / 1e3) if kms["nn"] > 0 else None,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "iterations": e2e_iters, "seconds": e2e_s},
+                    "iterations": e2e_iters, "seconds": e2e_s,
+                    "samples": e2e_samples, "note": "median of 3 one-shot nrr_register calls, fresh context each"},
             "gpu_launches": launches,
             "clocks": clocks.result(),
         }

@@ -11,6 +11,7 @@
 // any value. Energies use fixed-size grids and fixed reduction trees; each K/B
 // entry is summed by one lane in contributor (vertex) order.
 #include <cmath>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.cuh"
@@ -727,9 +728,14 @@ void launch_aa_update(const AADevice& aa, const double* g, const double* x, cons
 
 template <int K>
 static void aa_solve_k(const AADevice& aa, int D, const SlotList& cols, cudaStream_t s) {
-    // 32 CTAs x 256 threads: a few rows per thread, then log-depth merges
-    // (warp shuffles, CTA tree, one warp over the 32 CTA factors)
-    constexpr int kBlocks = 32;
+    // kBlocks CTAs x 256 threads: a few rows per thread, then log-depth
+    // merges (warp shuffles, CTA tree, one warp over the CTA factors); the
+    // CTA count trades the per-thread fold chain against the merge depth
+    static const int kBlocks = [] {
+        const char* e = std::getenv("NRR_AA_BLOCKS");
+        const int b = e ? std::atoi(e) : 32;
+        return b >= 1 && b <= 32 ? b : 32;
+    }();
     aa_tsqr_kernel<K><<<kBlocks, kTermThreads, 0, s>>>(aa, D, cols);
     aa_solve_kernel<K><<<1, 32, 0, s>>>(aa, static_cast<double>(D), kBlocks);
 }
