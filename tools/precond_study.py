@@ -111,10 +111,20 @@ def two_level(K, Mf, Z, mode="additive"):
     if mode == "additive":
         return lambda r: Mf(r) + Z @ (Ei @ (Z.T @ r))
 
-    def adef2(r):  # M^-1 (I - K Q) r + Q r
+    def adef1(r):  # M^-1 (I - K Q) r + Q r  (Tang et al. A-DEF1)
         y = Ei @ (Z.T @ r)
         return Mf(r - KZ @ y) + Z @ y
-    return adef2
+
+    def adef2(r):  # (I - Q K) M^-1 r + Q r  (Tang et al. A-DEF2): M^-1 r + Z E^-1 Z^T (r - K M^-1 r)
+        m = Mf(r)
+        return m + Z @ (Ei @ (Z.T @ (r - K @ m)))
+    return adef1 if mode == "adef1" else adef2
+
+
+def coarse_start(K, B, x0, Z):
+    """x0 + Q r0: the initial residual orthogonal to the coarse space (A-DEF2's start)"""
+    E = (Z.T @ K @ Z).toarray()
+    return x0 + Z @ sl.solve(E, Z.T @ (B - K @ x0), assume_a="pos")
 
 
 def main():
@@ -137,7 +147,9 @@ def main():
         aggs = [np.concatenate(subs[a * per:(a + 1) * per]) for a in range(nagg)]
         Z = affine_space(pos, aggs, N)
         res["BJ + additive affine x%d" % nagg] = pcg(K, B, x0, two_level(K, Mf, Z), rtol)[0]
+        res["BJ + ADEF1 affine x%d" % nagg] = pcg(K, B, x0, two_level(K, Mf, Z, "adef1"), rtol)[0]
         res["BJ + ADEF2 affine x%d" % nagg] = pcg(K, B, x0, two_level(K, Mf, Z, "adef2"), rtol)[0]
+        res["BJ + ADEF2 affine x%d, Q start" % nagg] = pcg(K, B, coarse_start(K, B, x0, Z), two_level(K, Mf, Z, "adef2"), rtol)[0]
     # overlapping subdomains (one ring of neighbours), additive Schwarz + affine x19
     nb = [set() for _ in range(N)]
     for a, b in p.graph.edges:
