@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnrr_b200.so")
+# NRR_LIB_PATH: an alternative build of this library (A/B experiments)
+LIB_PATH = os.environ.get("NRR_LIB_PATH") or os.path.join(_HERE, "libnrr_b200.so")
 
 i32p = C.POINTER(C.c_int32)
 f64p = C.POINTER(C.c_double)

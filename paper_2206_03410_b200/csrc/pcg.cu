@@ -1206,6 +1206,9 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
                 sh.zz[3 * i + 2] = a2;
             }
         }
+        // staged so that every thread stores its own elements of Z (coalesced):
+        // direct scattered stores by the q == 0 lanes (and no barrier here)
+        // measured +17% per PCG solve
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
@@ -1437,7 +1440,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             inv_gam[c] = gam[c] != 0.0 ? rcp_nr(gam[c]) : 0.0;
             if (al[c] != 0.0) inv_alp[c] = rcp_nr(al[c]);
         }
-        __syncthreads();  // ext reads done before precond_sub rewrites own rows
+        // (no CTA barrier: precond_sub's first barrier orders these ext reads
+        // before its own-row writes)
         cstop_t(1);
         mark(4);
     }
