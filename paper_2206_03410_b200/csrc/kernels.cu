@@ -390,224 +390,291 @@ __global__ void __launch_bounds__(kTermThreads) aa_update_kernel(AADevice aa, co
     }
 }
 
-// ---- TSQR of the tall-skinny [dF (newest first) | f] (D x K, K = mk+1) with
-// Givens rotations: every thread folds its rows into a K x K upper-triangular
-// R held in registers, then the R factors are merged pairwise in a fixed tree
-// (warp shuffles, shared memory, then one warp over the CTA partials). The
-// result is the R factor of a backward-stable QR of the whole matrix, from
-// which the reference's column-pivoted Householder QR (anderson.hpp:37-39) is
-// finished on a K x K problem: this keeps the QR's kappa*eps accuracy and
-// rank decision instead of the kappa^2*eps of normal equations.
 template <int K>
-struct Tri {
-    double r[K * (K + 1) / 2];  // row-major upper triangle
+struct Tri {  // packed row-major upper triangle
     __device__ __forceinline__ static int at(int i, int j) { return i * K - i * (i - 1) / 2 + (j - i); }
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int t = 0; t < K * (K + 1) / 2; ++t) r[t] = 0.0;
-    }
-    // fold the row a[k0..K) (entries before k0 are zero) into R
-    __device__ __forceinline__ void add_row(double* a, int k0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (k < k0) continue;
-            const double ak = a[k];
-            if (ak == 0.0) continue;
-            const double rk = r[at(k, k)];
-            // one reciprocal square root instead of sqrt + two divisions
-            // (the merge chains are latency-bound)
-            const double h2 = fma(rk, rk, ak * ak);
-            const double inv = rsqrt(h2);
-            const double c = rk * inv, s = ak * inv;
-            r[at(k, k)] = h2 * inv;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                if (j <= k) continue;
-                const double t = r[at(k, j)];
-                r[at(k, j)] = c * t + s * a[j];
-                a[j] = -s * t + c * a[j];
-            }
-        }
-    }
-    __device__ __forceinline__ void merge(const Tri& o) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            double a[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) a[j] = j < i ? 0.0 : o.r[at(i, j)];
-            add_row(a, i);
-        }
-    }
-    __device__ __forceinline__ void shfl_merge(int src_off) {  // merge lane+src_off's R into this lane's
-        Tri o;
-#pragma unroll
-        for (int t = 0; t < K * (K + 1) / 2; ++t) o.r[t] = __shfl_down_sync(0xffffffffu, r[t], src_off);
-        if ((threadIdx.x & (2 * src_off - 1)) == 0) merge(o);
-    }
 };
 
-template <int K>
-__global__ void __launch_bounds__(kTermThreads) aa_tsqr_kernel(AADevice aa, int D, SlotList cols) {
-    __shared__ double sR[kTermThreads / 32][K * (K + 1) / 2];
-    Tri<K> R;
-    R.zero();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
-        double a[K];
+// ---- Least squares min |f - dF theta| (anderson.hpp:36-44) from the R factor
+// of the tall-skinny [dF (newest first) | f] (D x K, K = mk+1), computed by a
+// communication-avoiding Householder QR: a warp holds a panel of rows (S per
+// lane) and reduces it to a K x K triangle with K reflections whose norms and
+// dot products are xor-butterfly sums (every lane gets the same bits, fixed
+// order: deterministic); triangles are stacked and reduced again (warp panels
+// -> one per CTA -> one). This keeps the QR's kappa*eps accuracy and rank
+// decision (normal equations would square kappa), and the critical path is
+// 3-4 panel factorisations of ~K butterfly rounds each instead of a 14-deep
+// tree of serial Givens merges (62 -> ~15 us per pass on config 2).
+
+// Householder QR of the S*32 rows a warp holds: lane l, slot s is one row;
+// row (slot 0, lane k) is the pivot row of column k. Afterwards lane k < K
+// holds row k of R in a[0][k..K) (entries left of the diagonal, and every
+// other row, are to be taken as zero).
+template <int K, int S>
+__device__ __forceinline__ void warp_house_qr(double (&a)[S][K]) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int j = 0; j < K - 1; ++j) a[j] = aa.df[static_cast<size_t>(cols.s[j]) * D + i];
-        a[K - 1] = aa.fprev[i];
-        R.add_row(a, 0);
-    }
+    for (int k = 0; k < K; ++k) {
+        // rows of slot 0 in lanes < k are finished rows of R
+        const bool live0 = lane > k;  // slot 0 is a non-pivot live row
+        double tail = live0 ? a[0][k] * a[0][k] : 0.0;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) R.shfl_merge(off);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (lane == 0)
+        for (int t = 1; t < S; ++t) tail = fma(a[t][k], a[t][k], tail);
+        tail = warp_sum(tail);
+        const double x0 = __shfl_sync(0xffffffffu, a[0][k], k);
+        if (!(tail > 2.2250738585072014e-308)) continue;  // nothing below the pivot (warp-uniform)
+        double beta = sqrt(fma(x0, x0, tail));
+        if (x0 >= 0) beta = -beta;
+        const double vp = x0 - beta;                    // pivot entry of v = x - beta e_p
+        const double d = 1.0 / (beta * (beta - x0));   // 2 / v^T v  (> 0)
+        const double v0 = lane == k ? vp : (live0 ? a[0][k] : 0.0);
+        double f[K];
 #pragma unroll
-        for (int t = 0; t < K * (K + 1) / 2; ++t) sR[w][t] = R.r[t];
-    __syncthreads();
-    // fixed binary tree over the warp factors (log2(nw) merges on the critical path)
-    for (int step = 1; step < nw; step <<= 1) {
-        if (lane == 0 && (w & (2 * step - 1)) == 0 && w + step < nw) {
-            Tri<K> o;
+        for (int j = k + 1; j < K; ++j) {
+            double dot = v0 * a[0][j];
 #pragma unroll
-            for (int t = 0; t < K * (K + 1) / 2; ++t) o.r[t] = sR[w + step][t];
-            R.merge(o);
-#pragma unroll
-            for (int t = 0; t < K * (K + 1) / 2; ++t) sR[w][t] = R.r[t];
+            for (int t = 1; t < S; ++t) dot = fma(a[t][k], a[t][j], dot);
+            f[j] = dot;
         }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0)
 #pragma unroll
-        for (int t = 0; t < K * (K + 1) / 2; ++t) aa.partials[static_cast<size_t>(blockIdx.x) * kTriMax + t] = R.r[t];
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int j = k + 1; j < K; ++j) f[j] += __shfl_xor_sync(0xffffffffu, f[j], o);
+#pragma unroll
+        for (int j = k + 1; j < K; ++j) {
+            const double fj = f[j] * d;
+            a[0][j] = fma(-v0, fj, a[0][j]);
+#pragma unroll
+            for (int t = 1; t < S; ++t) a[t][j] = fma(-a[t][k], fj, a[t][j]);
+        }
+        if (lane == k) a[0][k] = beta;
+    }
 }
 
-// Merge the CTA partials (one warp, fixed tree) and finish with the
-// reference's ColPivHouseholderQR semantics on the K x K factor: pivot on
-// the largest remaining column norm (norms downdated as Eigen does), rank =
-// #|R_kk| > |R|max * eps * min(D, mk); full rank -> back-substitution,
-// otherwise (dF^T dF + 1e-10 I) theta = dF^T f (anderson.hpp:41-43).
+constexpr int kAaWarps = kTermThreads / 32;
+// rows of a warp panel per lane besides the carried triangle (registers: (SN+1) K doubles)
 template <int K>
-__global__ void aa_solve_kernel(AADevice aa, double D, int nblocks) {
+struct AaPanel {
+    static constexpr int SN = K <= 6 ? 8 : (K <= 9 ? 4 : 2);
+    static constexpr int SM = (kAaWarps * K + 31) / 32;  // slots for the CTA's stacked warp triangles
+    static constexpr int SS = 4;                         // slots per lane in the final kernel
+};
+
+// The CTA's warp triangles (lane k < K of every warp: row k in r0[k..K)) are
+// stacked in shared memory and reduced by warp 0; returns (warp 0, lane k < K)
+// row k of the CTA's R in r0. sR: kAaWarps * K * K doubles.
+template <int K>
+__device__ __forceinline__ void block_merge_qr(double (&r0)[K], double* sR) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane < K)
+#pragma unroll
+        for (int j = 0; j < K; ++j) sR[(w * K + lane) * K + j] = j >= lane ? r0[j] : 0.0;
+    __syncthreads();
+    if (w != 0) return;
+    constexpr int SM = AaPanel<K>::SM;
+    double a[SM][K];
+#pragma unroll
+    for (int t = 0; t < SM; ++t) {
+        const int row = t * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < K; ++j) a[t][j] = row < kAaWarps * K ? sR[row * K + j] : 0.0;
+    }
+    warp_house_qr<K, SM>(a);
+#pragma unroll
+    for (int j = 0; j < K; ++j) r0[j] = a[0][j];
+}
+
+// Window push (solver.hpp:267-268, anderson.hpp:31-34) fused with the panel
+// factorisation: row i's new difference entries go to ring slot `slot`, the
+// residual f and g are stored, and the row [dF(cols) | f] joins the warp's
+// panel. Writes the CTA's triangle (packed rows) to aa.partials.
+template <int K>
+__global__ void __launch_bounds__(kTermThreads) aa_push_qr_kernel(AADevice aa, const double* __restrict__ g,
+                                                                  const double* __restrict__ x,
+                                                                  const double* __restrict__ f_in, int D,
+                                                                  int have_prev, int slot, SlotList cols) {
+    constexpr int SN = AaPanel<K>::SN;
+    __shared__ double sR[kAaWarps * K * K];
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * kAaWarps + (threadIdx.x >> 5), nwarps = gridDim.x * kAaWarps;
+    const int nchunks = (D + 32 * SN - 1) / (32 * SN);
+    double a[SN + 1][K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) a[0][j] = 0.0;
+    for (int chunk = gw; chunk < nchunks; chunk += nwarps) {
+#pragma unroll
+        for (int t = 1; t <= SN; ++t) {
+            const int i = (chunk * SN + (t - 1)) * 32 + lane;
+            if (i < D) {
+                const double gi = g[i];
+                const double f = f_in ? f_in[i] : gi - x[i];  // F = G - X
+                double dfn = 0.0;
+                if (have_prev) {
+                    dfn = f - aa.fprev[i];
+                    aa.df[static_cast<size_t>(slot) * D + i] = dfn;
+                    aa.dg[static_cast<size_t>(slot) * D + i] = gi - aa.gprev[i];
+                }
+                aa.fprev[i] = f;
+                aa.gprev[i] = gi;
+#pragma unroll
+                for (int j = 0; j < K - 1; ++j)
+                    a[t][j] = (have_prev && cols.s[j] == slot) ? dfn : aa.df[static_cast<size_t>(cols.s[j]) * D + i];
+                a[t][K - 1] = f;
+            } else {
+#pragma unroll
+                for (int j = 0; j < K; ++j) a[t][j] = 0.0;
+            }
+        }
+        warp_house_qr<K, SN + 1>(a);
+        // the carried triangle: row k in lane k, zero left of the diagonal; other lanes' slot 0 is spent
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (lane >= K || j < lane) a[0][j] = 0.0;
+    }
+    double r0[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) r0[j] = a[0][j];
+    block_merge_qr<K>(r0, sR);
+    if (threadIdx.x < K)
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (j >= lane) aa.partials[static_cast<size_t>(blockIdx.x) * kTriMax + Tri<K>::at(lane, j)] = r0[j];
+}
+
+// The reference's ColPivHouseholderQR semantics on the K x K factor, one
+// column per lane (lane mk: the right-hand side): pivot on the largest
+// remaining column norm (ties: first in the permuted order, norms downdated
+// as Eigen does), rank = #|R_kk| > |R|max * eps * min(D, mk); full rank ->
+// back-substitution, otherwise (dF^T dF + 1e-10 I) theta = dF^T f from the
+// unpivoted factor (anderson.hpp:41-43). r0: lane k < K holds row k of R.
+// sm: K*K doubles of shared memory. Called by one full warp.
+template <int K>
+__device__ __forceinline__ void aa_finish(const double (&r0)[K], AADevice aa, double D, double* sm) {
     constexpr int mk = K - 1;
-    Tri<K> R;
-    R.zero();
-    for (int b = threadIdx.x; b < nblocks; b += 32) {  // nblocks <= 32: one load per lane
-        Tri<K> o;
+    constexpr unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    if (lane < K)
 #pragma unroll
-        for (int t = 0; t < K * (K + 1) / 2; ++t) o.r[t] = aa.partials[static_cast<size_t>(b) * kTriMax + t];
-        R.merge(o);
-    }
+        for (int j = 0; j < K; ++j) sm[lane * K + j] = j >= lane ? r0[j] : 0.0;
+    __syncwarp();
+    double col[K];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) R.shfl_merge(off);
-    if (threadIdx.x != 0) return;
-    // dense copy: A = R[:, :mk] (K x mk), c = R[:, mk]
-    double A[K][mk > 0 ? mk : 1], c[K];
-    for (int i = 0; i < K; ++i) {
-        for (int j = 0; j < mk; ++j) A[i][j] = j >= i ? R.r[Tri<K>::at(i, j)] : 0.0;
-        c[i] = R.r[Tri<K>::at(i, mk)];
-    }
+    for (int i = 0; i < K; ++i) col[i] = lane < K ? sm[i * K + lane] : 0.0;
+    const bool iscol = lane < mk;
     const double eps = 2.220446049250313e-16;
-    double nu[mk > 0 ? mk : 1], nd[mk > 0 ? mk : 1];
-    int perm[mk > 0 ? mk : 1];
-    double maxnorm = 0.0;
-    for (int j = 0; j < mk; ++j) {
+    double nu, nd;
+    {
         double s = 0.0;
-        for (int i = 0; i < K; ++i) s += A[i][j] * A[i][j];
-        nu[j] = nd[j] = sqrt(s);
-        maxnorm = fmax(maxnorm, nu[j]);
-        perm[j] = j;
+#pragma unroll
+        for (int i = 0; i < K; ++i) s += col[i] * col[i];
+        nu = nd = iscol ? sqrt(s) : -1.0;
     }
+    const double maxnorm = warp_max(iscol ? nu : 0.0);
     const double thr_helper = (maxnorm * eps) * (maxnorm * eps) / D;
+    int pos = iscol ? lane : 64;  // position of the lane's column in the pivoted order
     int nonzero = mk;
     double maxpivot = 0.0;
+#pragma unroll
     for (int k = 0; k < mk; ++k) {
-        int best = k;
-        for (int j = k + 1; j < mk; ++j)
-            if (nu[j] > nu[best]) best = j;
-        if (nonzero == mk && nu[best] * nu[best] < thr_helper * (D - k)) nonzero = k;
-        if (best != k) {
-            for (int i = 0; i < K; ++i) {
-                const double t = A[i][k];
-                A[i][k] = A[i][best];
-                A[i][best] = t;
+        // largest remaining norm, ties to the smallest position
+        double bn = (iscol && pos >= k) ? nu : -1.0;
+        int bp = pos;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double on = __shfl_xor_sync(full, bn, o);
+            const int op = __shfl_xor_sync(full, bp, o);
+            if (on > bn || (on == bn && op < bp)) {
+                bn = on;
+                bp = op;
             }
-            double t = nu[k];
-            nu[k] = nu[best];
-            nu[best] = t;
-            t = nd[k];
-            nd[k] = nd[best];
-            nd[best] = t;
-            const int tp = perm[k];
-            perm[k] = perm[best];
-            perm[best] = tp;
         }
-        // Householder on A[k.., k]
+        bn = __shfl_sync(full, bn, 0);  // one decision for the warp (NaN norms compare inconsistently)
+        bp = __shfl_sync(full, bp, 0);
+        if (nonzero == mk && bn * bn < thr_helper * (D - k)) nonzero = k;
+        const bool is_piv = iscol && pos == bp;
+        if (iscol) {
+            if (pos == k)
+                pos = bp;
+            else if (pos == bp)
+                pos = k;
+        }
+        const unsigned pm = __ballot_sync(full, is_piv);
+        const int pl = pm ? __ffs(pm) - 1 : 0;
+        // Householder on the pivot column's entries k.. (every lane computes it)
         double tail = 0.0;
-        for (int i = k + 1; i < K; ++i) tail += A[i][k] * A[i][k];
-        const double c0 = A[k][k];
+#pragma unroll
+        for (int i = k + 1; i < K; ++i) tail += col[i] * col[i];
+        tail = __shfl_sync(full, tail, pl);
+        const double c0 = __shfl_sync(full, col[k], pl);
+        double ess[K];
         double tau = 0.0, beta = c0;
         if (tail > 2.2250738585072014e-308) {
             beta = sqrt(c0 * c0 + tail);
             if (c0 >= 0) beta = -beta;
-            for (int i = k + 1; i < K; ++i) A[i][k] /= (c0 - beta);
+#pragma unroll
+            for (int i = k + 1; i < K; ++i) ess[i] = __shfl_sync(full, col[i], pl) / (c0 - beta);
             tau = (beta - c0) / beta;
         } else {
-            for (int i = k + 1; i < K; ++i) A[i][k] = 0.0;
+#pragma unroll
+            for (int i = k + 1; i < K; ++i) ess[i] = 0.0;
         }
-        A[k][k] = beta;
         maxpivot = fmax(maxpivot, fabs(beta));
-        for (int j = k + 1; j < mk; ++j) {  // apply to remaining columns
-            double t = A[k][j];
-            for (int i = k + 1; i < K; ++i) t += A[i][k] * A[i][j];
-            A[k][j] -= tau * t;
-            for (int i = k + 1; i < K; ++i) A[i][j] -= tau * A[i][k] * t;
+        if ((iscol && pos > k) || lane == mk) {  // remaining columns and the right-hand side
+            double t = col[k];
+#pragma unroll
+            for (int i = k + 1; i < K; ++i) t += ess[i] * col[i];
+            col[k] -= tau * t;
+#pragma unroll
+            for (int i = k + 1; i < K; ++i) col[i] -= tau * ess[i] * t;
         }
-        {  // and to the rhs
-            double t = c[k];
-            for (int i = k + 1; i < K; ++i) t += A[i][k] * c[i];
-            c[k] -= tau * t;
-            for (int i = k + 1; i < K; ++i) c[i] -= tau * A[i][k] * t;
-        }
-        for (int j = k + 1; j < mk; ++j) {  // Eigen's norm downdate
-            if (nu[j] != 0.0) {
-                double t = fabs(A[k][j]) / nu[j];
-                t = (1.0 + t) * (1.0 - t);
-                t = t < 0 ? 0 : t;
-                const double rr = nu[j] / nd[j];
-                if (t * rr * rr <= sqrt(eps)) {
-                    double s = 0.0;
-                    for (int i = k + 1; i < K; ++i) s += A[i][j] * A[i][j];
-                    nu[j] = nd[j] = sqrt(s);
-                } else {
-                    nu[j] *= sqrt(t);
-                }
+        if (is_piv) col[k] = beta;
+        if (iscol && pos > k && nu != 0.0) {  // Eigen's norm downdate
+            double t = fabs(col[k]) / nu;
+            t = (1.0 + t) * (1.0 - t);
+            t = t < 0 ? 0 : t;
+            const double rr = nu / nd;
+            if (t * rr * rr <= sqrt(eps)) {
+                double s = 0.0;
+#pragma unroll
+                for (int i = k + 1; i < K; ++i) s += col[i] * col[i];
+                nu = nd = sqrt(s);
+            } else {
+                nu *= sqrt(t);
             }
         }
     }
     const double thr = maxpivot * eps * fmin(D, static_cast<double>(mk));
-    int rank = 0;
-    for (int k = 0; k < nonzero; ++k) rank += fabs(A[k][k]) > thr ? 1 : 0;
-    double theta[mk > 0 ? mk : 1];
+    double mydiag = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+        if (i == pos) mydiag = col[i];
+    const int rank = __popc(__ballot_sync(full, iscol && pos < nonzero && fabs(mydiag) > thr));
     if (rank == mk) {
-        double y[mk > 0 ? mk : 1];
-        for (int k = nonzero - 1; k >= 0; --k) {
-            double v = c[k];
-            for (int j = k + 1; j < nonzero; ++j) v -= A[k][j] * y[j];
-            y[k] = v / A[k][k];
+        // column-oriented back-substitution on the right-hand side lane
+        double theta = 0.0;
+#pragma unroll
+        for (int k = mk - 1; k >= 0; --k) {
+            const unsigned pm = __ballot_sync(full, iscol && pos == k);
+            const int pl = pm ? __ffs(pm) - 1 : 0;
+            const double y = __shfl_sync(full, col[k], mk) / __shfl_sync(full, col[k], pl);
+            if (lane == pl) theta = y;
+#pragma unroll
+            for (int i = 0; i < k; ++i) {
+                const double aik = __shfl_sync(full, col[i], pl);
+                if (lane == mk) col[i] -= aik * y;
+            }
         }
-        for (int k = 0; k < mk; ++k) theta[k] = 0.0;
-        for (int k = 0; k < nonzero; ++k) theta[perm[k]] = y[k];
-    } else {
+        if (iscol) aa.theta[lane] = theta;
+    } else if (lane == 0) {
         // normal equations from the unpivoted factor: dF^T dF = Rf^T Rf, dF^T f = Rf^T c
         double G[mk > 0 ? mk : 1][mk > 0 ? mk : 1], b[mk > 0 ? mk : 1];
         for (int a = 0; a < mk; ++a) {
             double sb = 0.0;
-            for (int t = 0; t <= a; ++t) sb += R.r[Tri<K>::at(t, a)] * R.r[Tri<K>::at(t, mk)];
+            for (int t = 0; t <= a; ++t) sb += sm[t * K + a] * sm[t * K + mk];
             b[a] = sb;
             for (int bb = 0; bb < mk; ++bb) {
                 double s = 0.0;
-                for (int t = 0; t <= min(a, bb); ++t) s += R.r[Tri<K>::at(t, a)] * R.r[Tri<K>::at(t, bb)];
+                for (int t = 0; t <= min(a, bb); ++t) s += sm[t * K + a] * sm[t * K + bb];
                 G[a][bb] = s + (a == bb ? 1e-10 : 0.0);
             }
         }
@@ -633,10 +700,42 @@ __global__ void aa_solve_kernel(AADevice aa, double D, int nblocks) {
             for (int t = k + 1; t < mk; ++t) v -= G[t][k] * y[t];
             y[k] = v / G[k][k];
         }
-        for (int k = 0; k < mk; ++k) theta[k] = y[k];
+        for (int k = 0; k < mk; ++k) aa.theta[k] = y[k];
     }
-    for (int k = 0; k < mk; ++k) aa.theta[k] = theta[k];
-    *aa.rank = rank;
+    if (lane == 0) *aa.rank = rank;
+}
+
+// One CTA: the nblocks CTA triangles (nblocks * K stacked rows) are reduced
+// to one (a single warp panel when they fit AaPanel::SS slots, otherwise one
+// panel per warp and a second level) and the least squares finished.
+template <int K>
+__global__ void __launch_bounds__(kTermThreads) aa_solve_kernel(AADevice aa, double D, int nblocks) {
+    constexpr int SS = AaPanel<K>::SS;
+    __shared__ double sR[kAaWarps * K * K];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int rows = nblocks * K;
+    const bool single = rows <= 32 * SS;
+    if (single && w != 0) return;
+    const int per_warp = single ? rows : (rows + kAaWarps - 1) / kAaWarps;  // <= 32 * SS (launch_aa_solve)
+    const int row0 = single ? 0 : w * per_warp, row1 = min(rows, row0 + per_warp);
+    double a[SS][K];
+#pragma unroll
+    for (int t = 0; t < SS; ++t) {
+        const int row = row0 + t * 32 + lane;
+        const int b = row / K, i = row - b * K;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            a[t][j] = (row < row1 && j >= i) ? aa.partials[static_cast<size_t>(b) * kTriMax + Tri<K>::at(i, j)] : 0.0;
+    }
+    warp_house_qr<K, SS>(a);
+    double r0[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) r0[j] = a[0][j];
+    if (!single) {
+        block_merge_qr<K>(r0, sR);
+        if (w != 0) return;
+    }
+    aa_finish<K>(r0, aa, D, sR);
 }
 
 __global__ void __launch_bounds__(256) aa_combine_kernel(AADevice aa, int D, SlotList cols,
@@ -727,24 +826,30 @@ void launch_aa_update(const AADevice& aa, const double* g, const double* x, cons
 }
 
 template <int K>
-static void aa_solve_k(const AADevice& aa, int D, const SlotList& cols, cudaStream_t s) {
-    // kBlocks CTAs x 256 threads: a few rows per thread, then log-depth
-    // merges (warp shuffles, CTA tree, one warp over the CTA factors); the
-    // CTA count trades the per-thread fold chain against the merge depth
-    static const int kBlocks = [] {
+static void aa_push_solve_k(const AADevice& aa, const double* g, const double* x, const double* f, int D,
+                            int have_prev, int slot, const SlotList& cols, cudaStream_t s) {
+    // one warp panel of 32 * SN rows per warp and pass; the CTA count is
+    // bounded by the SMs and by the final kernel's capacity (kAaWarps panels
+    // of 32 * SS stacked triangle rows)
+    constexpr int SN = AaPanel<K>::SN;
+    const int nchunks = (D + 32 * SN - 1) / (32 * SN);
+    static const int kMaxBlocks = [] {
         const char* e = std::getenv("NRR_AA_BLOCKS");
-        const int b = e ? std::atoi(e) : 32;
-        return b >= 1 && b <= 32 ? b : 32;
+        const int b = e ? std::atoi(e) : 148;
+        return b >= 1 && b <= kTermBlocks ? b : 148;
     }();
-    aa_tsqr_kernel<K><<<kBlocks, kTermThreads, 0, s>>>(aa, D, cols);
-    aa_solve_kernel<K><<<1, 32, 0, s>>>(aa, static_cast<double>(D), kBlocks);
+    const int cap = (kAaWarps * 32 * AaPanel<K>::SS) / K;
+    const int blocks = std::max(1, std::min(std::min(kMaxBlocks, cap), (nchunks + kAaWarps - 1) / kAaWarps));
+    aa_push_qr_kernel<K><<<blocks, kTermThreads, 0, s>>>(aa, g, x, f, D, have_prev, slot, cols);
+    aa_solve_kernel<K><<<1, kTermThreads, 0, s>>>(aa, static_cast<double>(D), blocks);
 }
 
-void launch_aa_solve(const AADevice& aa, int D, const SlotList& cols, cudaStream_t s) {
+void launch_aa_push_solve(const AADevice& aa, const double* g, const double* x, const double* f, int D, int have_prev,
+                          int slot, const SlotList& cols, cudaStream_t s) {
     switch (cols.n + 1) {
 #define NRR_AA_CASE(k) \
     case k:            \
-        aa_solve_k<k>(aa, D, cols, s); \
+        aa_push_solve_k<k>(aa, g, x, f, D, have_prev, slot, cols, s); \
         break;
         NRR_AA_CASE(2) NRR_AA_CASE(3) NRR_AA_CASE(4) NRR_AA_CASE(5) NRR_AA_CASE(6) NRR_AA_CASE(7)
         NRR_AA_CASE(8) NRR_AA_CASE(9) NRR_AA_CASE(10) NRR_AA_CASE(11) NRR_AA_CASE(12) NRR_AA_CASE(13)

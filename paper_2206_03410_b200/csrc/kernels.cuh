@@ -102,8 +102,10 @@ struct SlotList {  // ring slots, newest first
 // into ring slot `slot` when the window held an entry (anderson.hpp:58-61)
 void launch_aa_update(const AADevice& aa, const double* g, const double* x, const double* f, int D, int have_prev,
                       int slot, cudaStream_t s);
-// least squares min |f - dF theta| over the columns `cols` (anderson.hpp:36-44)
-void launch_aa_solve(const AADevice& aa, int D, const SlotList& cols, cudaStream_t s);
+// the push fused with the least squares min |f - dF theta| over the columns
+// `cols` (anderson.hpp:31-44): theta and rank are left in aa.theta / aa.rank
+void launch_aa_push_solve(const AADevice& aa, const double* g, const double* x, const double* f, int D, int have_prev,
+                          int slot, const SlotList& cols, cudaStream_t s);
 // x_next = g - sum_j theta_j dg_{cols[j]} (anderson.hpp:45)
 void launch_aa_combine(const AADevice& aa, int D, const SlotList& cols, double* x_next, int* nonfinite,
                        cudaStream_t s);

@@ -869,14 +869,14 @@ void aa_push_combine(nrr_ctx* c, Window& w, const double* g, const double* x, co
     }
     w.hist = std::min(w.hist + 1, w.m + 1);
     const SlotList cols = to_slots(w.cols);
-    launch_aa_update(c->aa, g, x, f, D, have_prev, slot < 0 ? 0 : slot, c->stream);
-    ++c->launches;
     const int mk = std::min(w.hist - 1, w.m);
     if (mk <= 0) {
+        launch_aa_update(c->aa, g, x, f, D, have_prev, slot < 0 ? 0 : slot, c->stream);
+        ++c->launches;
         NRR_CUDA_CHECK(cudaMemcpyAsync(x_next, g, sizeof(double) * D, cudaMemcpyDeviceToDevice, c->stream));
         return;
     }
-    launch_aa_solve(c->aa, D, cols, c->stream);
+    launch_aa_push_solve(c->aa, g, x, f, D, have_prev, slot < 0 ? 0 : slot, cols, c->stream);
     launch_aa_combine(c->aa, D, cols, x_next, &c->d_rec.p->nonfinite, c->stream);
     c->launches += 3;
 }
