@@ -502,27 +502,44 @@ __global__ void __launch_bounds__(kTermThreads) aa_push_qr_kernel(AADevice aa, c
 #pragma unroll
     for (int j = 0; j < K; ++j) a[0][j] = 0.0;
     for (int chunk = gw; chunk < nchunks; chunk += nwarps) {
+        // every load of the panel is issued before the first store (the
+        // ring columns may alias for the compiler: interleaved, each slot
+        // cost its own DRAM round trip)
+        double gi[SN], fv[SN], fp[SN], gp[SN];
+#pragma unroll
+        for (int t = 1; t <= SN; ++t) {
+            const int i = (chunk * SN + (t - 1)) * 32 + lane;
+            gi[t - 1] = fv[t - 1] = fp[t - 1] = gp[t - 1] = 0.0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) a[t][j] = 0.0;
+            if (i < D) {
+                gi[t - 1] = g[i];
+                fv[t - 1] = f_in ? f_in[i] : x[i];
+                if (have_prev) {
+                    fp[t - 1] = aa.fprev[i];
+                    gp[t - 1] = aa.gprev[i];
+                }
+#pragma unroll
+                for (int j = 0; j < K - 1; ++j)
+                    if (!(have_prev && cols.s[j] == slot)) a[t][j] = aa.df[static_cast<size_t>(cols.s[j]) * D + i];
+            }
+        }
 #pragma unroll
         for (int t = 1; t <= SN; ++t) {
             const int i = (chunk * SN + (t - 1)) * 32 + lane;
             if (i < D) {
-                const double gi = g[i];
-                const double f = f_in ? f_in[i] : gi - x[i];  // F = G - X
-                double dfn = 0.0;
+                const double f = f_in ? fv[t - 1] : gi[t - 1] - fv[t - 1];  // F = G - X
                 if (have_prev) {
-                    dfn = f - aa.fprev[i];
+                    const double dfn = f - fp[t - 1];
                     aa.df[static_cast<size_t>(slot) * D + i] = dfn;
-                    aa.dg[static_cast<size_t>(slot) * D + i] = gi - aa.gprev[i];
+                    aa.dg[static_cast<size_t>(slot) * D + i] = gi[t - 1] - gp[t - 1];
+#pragma unroll
+                    for (int j = 0; j < K - 1; ++j)
+                        if (cols.s[j] == slot) a[t][j] = dfn;
                 }
                 aa.fprev[i] = f;
-                aa.gprev[i] = gi;
-#pragma unroll
-                for (int j = 0; j < K - 1; ++j)
-                    a[t][j] = (have_prev && cols.s[j] == slot) ? dfn : aa.df[static_cast<size_t>(cols.s[j]) * D + i];
+                aa.gprev[i] = gi[t - 1];
                 a[t][K - 1] = f;
-            } else {
-#pragma unroll
-                for (int j = 0; j < K; ++j) a[t][j] = 0.0;
             }
         }
         warp_house_qr<K, SN + 1>(a);

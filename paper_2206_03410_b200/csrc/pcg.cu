@@ -57,6 +57,13 @@ constexpr int kQ = kPcgSlots;  // partial slots per CTA and phase
 #define NRR_PCG_PROBES 0
 #endif
 constexpr bool kPcgProbes = NRR_PCG_PROBES != 0;
+// subdomain preconditioner matvec: one thread per output element (see
+// precond_sub) when a thread owns several elements (EPT >= 2: config 4
+// 7.09 -> 6.39 ms per solve), four threads per scalar row with a butterfly
+// for EPT = 1 (config 2: 0.847 vs 0.879 ms); 1 forces the former everywhere
+#ifndef NRR_PCG_DIRECT
+#define NRR_PCG_DIRECT 0
+#endif
 constexpr int kCoarseThreads = 512;
 
 // coarse mode k of node a in aggregate g: [e_k; d_k] for k < 3, e_3 for k = 3,
@@ -1162,6 +1169,45 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     // with_partials: the iteration partials were staged with the input; their
     // CTA reduction shares this routine's first barrier
     auto precond_sub = [&](const double (&v)[EPT], bool with_partials) {
+        if constexpr (NRR_PCG_DIRECT != 0 || EPT >= 2) {
+        // every thread forms its own elements' m' = (M_sub v)_e: the input is
+        // staged column-major by right-hand side (rexT[c][scalar row], leading
+        // dimension = 2 mod 16 doubles so the three columns' 16-byte loads hit
+        // distinct banks), M_sub rows and the input are read with 16-byte
+        // loads, four independent chains; no partial-sum shuffles, no second
+        // staging buffer and no second barrier
+        double* rexT = sh.zz;  // zz and rex are contiguous: 24 max_rows doubles
+        const int ldr = 4 * a.max_rows + 2;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k)
+            if (el_row[k] >= 0) rexT[my_c * ldr + 4 * el_row[k] + my_r] = v[k];
+        __syncthreads();
+        if (with_partials) partials_reduce(a.use_coarse ? 19 : 7, sh.red, a.part_a + pph * a.part_stride);
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            if (el_row[k] < 0) continue;
+            const int lr = el_row[k];
+            const int ch = sh.rchunk[lr], st = sh.cstart[ch];
+            const int nk = 4 * (sh.cstart[ch + 1] - st);
+            const double2* m = reinterpret_cast<const double2*>(sh.Minv + ch * sub_msz +
+                                                                static_cast<size_t>(4 * (lr - st) + my_r) * sub_ld);
+            const double2* rv = reinterpret_cast<const double2*>(rexT + my_c * ldr + 4 * st);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 4
+            for (int j = 0; j < nk / 2; j += 2) {
+                const double2 m01 = m[j], m23 = m[j + 1];
+                const double2 r01 = rv[j], r23 = rv[j + 1];
+                a0 = fma(m01.x, r01.x, a0);
+                a1 = fma(m01.y, r01.y, a1);
+                a2 = fma(m23.x, r23.x, a2);
+                a3 = fma(m23.y, r23.y, a3);
+            }
+            const double z = (a0 + a1) + (a2 + a3);
+            __stcg(a.Z + zph * a.z_stride + el_g[k], z);
+            sh.ext[lr * 12 + my_rc] = z;
+        }
+        return;
+        }
 #pragma unroll
         for (int k = 0; k < EPT; ++k)
             if (el_row[k] >= 0) sh.rex[el_row[k] * 12 + my_rc] = v[k];
