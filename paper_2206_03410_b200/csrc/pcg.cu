@@ -648,6 +648,8 @@ struct Shared {
     double* red;     // kRedDoubles: reduction scratch
     double* bcast;   // kQ
     double* ext;     // (own rows + halo) x 12: the SpMV operand staged from L2
+    int* rp;         // max_rows + 1: block range starts of the own rows, relative to the CTA's first block
+    int* rnode;      // max_rows: node id of the own rows
 };
 
 __device__ __forceinline__ double op2(bool mx, double a, double b) { return mx ? fmax(a, b) : a + b; }
@@ -940,6 +942,10 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         p += (a.max_rows + 1) / 2;
         sh.tl = reinterpret_cast<int*>(p);
         p += (a.max_ext + 1) / 2;
+        sh.rp = reinterpret_cast<int*>(p);
+        p += (a.max_rows + 2) / 2;
+        sh.rnode = reinterpret_cast<int*>(p);
+        p += (a.max_rows + 1) / 2;
         if ((p - reinterpret_cast<double*>(smem_raw)) & 1) ++p;  // 16-byte aligned K
         if (a.k_in_smem) {
             sh.K = p;
@@ -964,6 +970,10 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             const int t = i / (4 * nc), kj = i - t * 4 * nc;
             sh.cinv[i] = a.coarse_inv[static_cast<size_t>(a.touch_agg[t0 + t]) * 4 * nc + kj];
         }
+    }
+    for (int lr = threadIdx.x; lr <= nrows; lr += blockDim.x) {
+        sh.rp[lr] = a.row_ptr[r0 + lr] - kb0;
+        if (lr < nrows) sh.rnode[lr] = a.row_node[r0 + lr];
     }
     for (int e = threadIdx.x; e < n_ext; e += blockDim.x) {
         double d3[3];
@@ -1027,20 +1037,42 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     // local memory).
     const int nel = nrows * 12;
     const int my_rc = threadIdx.x % 12, my_r = my_rc / 3, my_c = my_rc % 3;
-    double xr[EPT], rr[EPT], ur[EPT], wr[EPT], pr[EPT], sr[EPT], qr[EPT], zv[EPT];  // B is re-read at a restart
-    int el_row[EPT], el_b0[EPT], el_b1[EPT];  // row, block range in the CTA's K
-    size_t el_g[EPT];
+    // kLean (4 or more elements per thread): x and the search direction p only
+    // accumulate (nothing else in the iteration reads them), so they live in
+    // global memory (X itself and the scratch P) instead of 4 registers per
+    // element
+    constexpr bool kLean = EPT >= 4;
+    constexpr int kXp = kLean ? 1 : EPT;
+    double xr[kXp], pr[kXp];
+    double rr[EPT], ur[EPT], wr[EPT], sr[EPT], qr[EPT], zv[EPT];  // B is re-read at a restart
+    // With 4 or more elements per thread the block ranges and global offsets
+    // are looked up in shared memory (rp / rnode) instead of held in
+    // registers: 5 registers per element, which pcg_kernel<4> spilled
+    constexpr int kIdx = kLean ? 1 : EPT;
+    int el_row[EPT], el_b0[kIdx], el_b1[kIdx];  // row, block range in the CTA's K
+    size_t el_gr[kIdx];
+    auto el_g = [&](int k) -> size_t {
+        if constexpr (kLean)
+            return static_cast<size_t>(sh.rnode[el_row[k]]) * 12 + my_rc;
+        else
+            return el_gr[k];
+    };
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
         const int e = threadIdx.x + k * blockDim.x;
         const bool live = e < nel;
         const int lr = live ? e / 12 : 0;
         el_row[k] = live ? lr : -1;
-        el_b0[k] = a.row_ptr[r0 + lr] - kb0;
-        el_b1[k] = live ? a.row_ptr[r0 + lr + 1] - kb0 : el_b0[k];
-        el_g[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + my_rc;
-        xr[k] = live ? a.X[el_g[k]] : 0.0;
-        rr[k] = ur[k] = wr[k] = pr[k] = sr[k] = qr[k] = zv[k] = 0.0;
+        if constexpr (!kLean) {
+            el_b0[k] = a.row_ptr[r0 + lr] - kb0;
+            el_b1[k] = live ? a.row_ptr[r0 + lr + 1] - kb0 : el_b0[k];
+            el_gr[k] = static_cast<size_t>(a.row_node[r0 + lr]) * 12 + my_rc;
+        }
+        if constexpr (!kLean) {
+            xr[k] = live ? a.X[el_g(k)] : 0.0;
+            pr[k] = 0.0;
+        }
+        rr[k] = ur[k] = wr[k] = sr[k] = qr[k] = zv[k] = 0.0;
     }
 
     // Parities of the exchanged vector Z and of the iteration partials: every
@@ -1076,7 +1108,15 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         __syncthreads();
     };
     auto spmv = [&](int k) -> double {
-        const int b0 = el_b0[k], b1 = el_b1[k];  // empty range for dead elements
+        int b0, b1;  // empty range for dead elements
+        if constexpr (kLean) {
+            const int lr = el_row[k];
+            b0 = lr >= 0 ? sh.rp[lr] : 0;
+            b1 = lr >= 0 ? sh.rp[lr + 1] : 0;
+        } else {
+            b0 = el_b0[k];
+            b1 = el_b1[k];
+        }
         // four independent chains, all of a group's loads issued before its
         // FMAs (K comes from L2 when it does not fit in shared memory)
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
@@ -1203,7 +1243,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
                 a3 = fma(m23.y, r23.y, a3);
             }
             const double z = (a0 + a1) + (a2 + a3);
-            __stcg(a.Z + zph * a.z_stride + el_g[k], z);
+            __stcg(a.Z + zph * a.z_stride + el_g(k), z);
             sh.ext[lr * 12 + my_rc] = z;
         }
         return;
@@ -1260,7 +1300,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         for (int k = 0; k < EPT; ++k) {
             if (el_row[k] < 0) continue;
             const double z = sh.zz[el_row[k] * 12 + my_rc];
-            __stcg(a.Z + zph * a.z_stride + el_g[k], z);
+            __stcg(a.Z + zph * a.z_stride + el_g(k), z);
             sh.ext[el_row[k] * 12 + my_rc] = z;
         }
     };
@@ -1347,15 +1387,19 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
 #pragma unroll
             for (int k = 0; k < EPT; ++k)
                 if (el_row[k] >= 0) {
-                    __stcg(a.X + el_g[k], xr[k]);
-                    sh.ext[el_row[k] * 12 + my_rc] = xr[k];
+                    if constexpr (kLean) {
+                        sh.ext[el_row[k] * 12 + my_rc] = __ldcg(a.X + el_g(k));
+                    } else {
+                        __stcg(a.X + el_g(k), xr[k]);
+                        sh.ext[el_row[k] * 12 + my_rc] = xr[k];
+                    }
                 }
             grid.sync();
             exchange(a.X, false);
             double rmx = 0.0, bmx = 0.0, ps[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
-                const double bk = el_row[k] >= 0 ? __ldg(a.B + el_g[k]) : 0.0;
+                const double bk = el_row[k] >= 0 ? __ldg(a.B + el_g(k)) : 0.0;
                 rr[k] = bk - spmv(k);
                 if (el_row[k] < 0) continue;
                 rmx = fmax(rmx, fabs(rr[k]));
@@ -1397,7 +1441,12 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             for (int k = 0; k < EPT; ++k) {
                 ur[k] = el_row[k] >= 0 ? sh.ext[el_row[k] * 12 + my_rc] : 0.0;
                 wr[k] = spmv(k);
-                pr[k] = sr[k] = qr[k] = zv[k] = 0.0;
+                sr[k] = qr[k] = zv[k] = 0.0;
+                if constexpr (kLean) {
+                    if (el_row[k] >= 0) __stcg(a.P + el_g(k), 0.0);
+                } else {
+                    pr[k] = 0.0;
+                }
             }
             first = true;
             need_init = false;
@@ -1469,12 +1518,25 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
             for (int k = 0; k < EPT; ++k) {
                 if (el_row[k] < 0) continue;
                 const double m = sh.ext[el_row[k] * 12 + my_rc];
+                double p_old = 0.0, x_old = 0.0;
+                size_t g = 0;
+                if constexpr (kLean) {  // in flight during this element's SpMV
+                    g = el_g(k);
+                    p_old = __ldcg(a.P + g);
+                    x_old = __ldcg(a.X + g);
+                }
                 const double n = spmv(k);
                 zv[k] = fma(b_c, zv[k], n);
                 qr[k] = fma(b_c, qr[k], m);
                 sr[k] = fma(b_c, sr[k], wr[k]);
-                pr[k] = fma(b_c, pr[k], ur[k]);
-                xr[k] = fma(a_c, pr[k], xr[k]);
+                if constexpr (kLean) {
+                    const double pn = fma(b_c, p_old, ur[k]);
+                    __stcg(a.P + g, pn);
+                    __stcg(a.X + g, fma(a_c, pn, x_old));
+                } else {
+                    pr[k] = fma(b_c, pr[k], ur[k]);
+                    xr[k] = fma(a_c, pr[k], xr[k]);
+                }
                 rr[k] = fma(-a_c, sr[k], rr[k]);
                 ur[k] = fma(-a_c, qr[k], ur[k]);
                 wr[k] = fma(-a_c, zv[k], wr[k]);
@@ -1493,7 +1555,8 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
     }
 #pragma unroll
     for (int k = 0; k < EPT; ++k)
-        if (el_row[k] >= 0) a.X[el_g[k]] = xr[k];
+        if constexpr (!kLean)
+            if (el_row[k] >= 0) a.X[el_g(k)] = xr[k];
     if (prof)
         for (int k = 0; k < 8; ++k) a.prof[k] += acc_t[k];
     if (prof)
@@ -1667,7 +1730,8 @@ void PcgPlan::size_smem(const int* row_ptr_solver, const int* col, size_t smem_l
                          12 * static_cast<size_t>(max_rows) /* rex */ + 3 * static_cast<size_t>(max_ext) /* offx */ +
                          (use_coarse ? 4 * max_touch * nc : 0) /* cinv */ + 12 * static_cast<size_t>(max_touch) +
                          3 * kCoarseMax /* ptq */ + 12 * static_cast<size_t>(max_ext) /* ext */ +
-                         (max_rows + 1) / 2 /* rchunk */ + (max_ext + 1) / 2 /* tl */ + 2;
+                         (max_rows + 1) / 2 /* rchunk */ + (max_ext + 1) / 2 /* tl */ + (max_rows + 2) / 2 /* rp */ +
+                         (max_rows + 1) / 2 /* rnode */ + 2;
     const size_t kbytes = static_cast<size_t>(max_kb) * (16 * sizeof(double) + sizeof(int));
     // largest subdomain chunk (rows per dense block-Jacobi inverse) that fits
     auto sub_doubles = [&](int S) {

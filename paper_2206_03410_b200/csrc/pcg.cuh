@@ -47,6 +47,7 @@ struct PcgArgs {
     const double* B;      // 12N node-major (by node id)
     double* X;            // 12N node-major: in = warm start, out = solution
     double* Z;            // 2 x 12N scratch (preconditioned residual, exchanged), two parities
+    double* P;            // 12N scratch: the search direction when a thread owns 4 or more elements (pcg.cu kLean)
     size_t z_stride;      // doubles between the parities of Z (>= 12N)
     const int* row_begin; // grid+1
     const double* node_pos;  // N*3

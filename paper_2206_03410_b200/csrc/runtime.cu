@@ -745,7 +745,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     // state buffers
     const size_t D = 12 * static_cast<size_t>(N);
     for (auto* b : {&c->x, &c->xmm, &c->xmm_spec, &c->xnext, &c->B}) b->resize(std::max<size_t>(D, 1));
-    c->Z.resize(2 * std::max<size_t>(D, 1));  // two parities (pcg.cu: exchanged vector, see PcgArgs::z_stride)
+    c->Z.resize(3 * std::max<size_t>(D, 1));  // + the PCG's search-direction scratch (PcgArgs::P)
+    c->Z.zero(s);  // two parities (pcg.cu: exchanged vector, see PcgArgs::z_stride)
     c->d_skip.resize(1);
     for (auto* b : {&c->vhat, &c->vhat2, &c->q}) b->resize(std::max<size_t>(3 * static_cast<size_t>(n), 1));
     c->d2.resize(std::max(n, 1));
@@ -1057,6 +1058,7 @@ void solve(nrr_ctx* c, const double* x0, double* xout) {
     a.B = c->B.p;
     a.X = xout;
     a.Z = c->Z.p;
+    a.P = c->Z.p + 2 * std::max<size_t>(12 * static_cast<size_t>(c->N), 1);
     a.z_stride = std::max<size_t>(12 * static_cast<size_t>(c->N), 1);
     a.part_stride = 8 * kPcgSlots * static_cast<size_t>((c->plan.grid + 7) & ~7);
     a.row_begin = c->row_begin.p;
