@@ -230,23 +230,48 @@ __global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __res
             const float r2 = r * r;
             double my_d2 = best_d2;
             int my_i = best_i;
-            const int ncell = cx * cy * cz;
-            for (int c = lane; c < ncell; c += 8) {
-                const int iz = c % cz, t = c / cz, iy = t % cy, ix = t / cy;
-                const int cell = ((x0 + ix) * bv.gny + (y0 + iy)) * bv.gnz + (z0 + iz);
-                const int p0 = bv.cell_start[cell], p1 = bv.cell_start[cell + 1];
-                for (int k = p0; k < p1; ++k) {
-                    const float4 pt = bv.gpts[k];
-                    const float dx = pt.x - fx, dy = pt.y - fy, dz = pt.z - fz;
-                    if (dx * dx + dy * dy + dz * dz > r2) continue;
-                    int idx;
-                    memcpy(&idx, &pt.w, 4);
-                    const double d2 = exact_d2(bv.tgt64 + 3 * idx, qx, qy, qz);
-                    if (d2 < my_d2 || (d2 == my_d2 && idx < my_i)) {
-                        my_d2 = d2;
-                        my_i = idx;
+            // The cells of one (x, y) column of the ball are consecutive in
+            // the cell-major point array, so a column is one contiguous run
+            // [cell_start[first], cell_start[last + 1]): two index loads per
+            // column instead of two per cell, and the run's points share
+            // sectors. A lane takes columns lane, lane + 8, ...; the ranges of
+            // two columns and the points of a run (4 at a time) are loaded
+            // before they are used, so the dependent chain is ranges -> points
+            // -> (rarely) the FP64 coordinates of a candidate.
+            auto scan = [&](int p0, int p1) {
+                for (int k = p0; k < p1; k += 4) {
+                    float4 pt[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) pt[u] = k + u < p1 ? bv.gpts[k + u] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (k + u >= p1) break;
+                        const float dx = pt[u].x - fx, dy = pt[u].y - fy, dz = pt[u].z - fz;
+                        if (dx * dx + dy * dy + dz * dz > r2) continue;
+                        int idx;
+                        memcpy(&idx, &pt[u].w, 4);
+                        const double d2 = exact_d2(bv.tgt64 + 3 * idx, qx, qy, qz);
+                        if (d2 < my_d2 || (d2 == my_d2 && idx < my_i)) {
+                            my_d2 = d2;
+                            my_i = idx;
+                        }
                     }
                 }
+            };
+            const int ncol = cx * cy;
+            for (int c = lane; c < ncol; c += 16) {
+                const int iy = c % cy, ix = c / cy;
+                const int cell = ((x0 + ix) * bv.gny + (y0 + iy)) * bv.gnz + z0;
+                const int p0 = bv.cell_start[cell], p1 = bv.cell_start[cell + cz];
+                int q0 = 0, q1 = 0;
+                if (c + 8 < ncol) {
+                    const int c2 = c + 8, jy = c2 % cy, jx = c2 / cy;
+                    const int cell2 = ((x0 + jx) * bv.gny + (y0 + jy)) * bv.gnz + z0;
+                    q0 = bv.cell_start[cell2];
+                    q1 = bv.cell_start[cell2 + cz];
+                }
+                scan(p0, p1);
+                scan(q0, q1);
             }
 #pragma unroll
             for (int o = 4; o > 0; o >>= 1) {
