@@ -420,7 +420,7 @@ void set_target(nrr_ctx* c, const double* tgt, int m) {
         const char* ge = std::getenv("NRR_NN_GRID");
         const char* gh = std::getenv("NRR_NN_GRID_H");
         const GridDims g = (ge && std::atoi(ge) == 0) ? GridDims{}
-                                                      : grid_dims(c->bvh.lo, c->bvh.hi, m, gh ? std::atof(gh) : 1.0);
+                                                      : grid_dims(c->bvh.lo, c->bvh.hi, m, gh ? std::atof(gh) : 0.85);
         if (g.nx > 0) {
             const long long ncells = static_cast<long long>(g.nx) * g.ny * g.nz;
             c->d_gpts.resize(m);
@@ -439,9 +439,10 @@ void set_target(nrr_ctx* c, const double* tgt, int m) {
             b.glz = static_cast<float>(c->bvh.lo[2] - c->bvh.center[2]);
             b.inv_h = static_cast<float>(1.0 / g.h);
             const char* gc = std::getenv("NRR_NN_GRID_CELLS");
-            // cell size factor 1.0 and <= 500 cells per grid-path query: NN
-            // -16% on config 2, -12% on config 4 against 1.4 / 216
-            // (profiles/r02_sweep_nn_c3_b.txt)
+            // cell size factor 0.85 (with the column-run scan: config 2 NN
+            // 49 -> 47 us, config 4 594 -> 547 us against 1.0,
+            // profiles/r04_nn_grid_sweep.txt) and <= 500 cells per grid-path
+            // query (profiles/r02_sweep_nn_c3_b.txt)
             b.gmax_cells = gc ? std::atoi(gc) : 500;
         }
     }
