@@ -238,6 +238,19 @@ def test_anderson_parity(ctx):
         assert np.max(np.abs(xg - xo)) <= 1e-9 * (1 + np.max(np.abs(xo)))
 
 
+@pytest.mark.parametrize("dim,h,m", [(250000, 6, 5), (40000, 12, 10), (3000, 18, 16), (12 * 3029, 9, 8)])
+def test_anderson_parity_panels(ctx, dim, h, m):
+    """The panel QR's other shapes: several panels per warp and the two-level
+    final kernel (large dim), the narrower panels of wide windows (m = 8..16)."""
+    rng = np.random.default_rng(dim + m)
+    G = rng.normal(size=(h, dim))
+    F = rng.normal(size=(h, dim)) * np.linspace(1.0, 1e-3, h)[:, None]  # graded columns: pivoting matters
+    xg, rg = ctx.anderson_combine(G, F, m)
+    xo, ro = O.anderson_combine(G, F, m)
+    assert rg == ro
+    assert np.max(np.abs(xg - xo)) <= 1e-9 * (1 + np.max(np.abs(xo)))
+
+
 def test_anderson_degenerate_falls_back(ctx):
     """solver_tests.cpp:82-92: zero difference columns -> Tikhonov, finite."""
     G = np.array([[1.0, -1.0]] * 3)
