@@ -1626,7 +1626,144 @@ void rcb(RcbCtx& ctx, int lo, int hi, int g0, int g1) {
 
 }  // namespace
 
-void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit) {
+// Lloyd relaxation of the bisection's subdomains: every node moves to the
+// nearest centroid among its own and its graph neighbours' subdomains that
+// still has room (at most `cap` nodes each; nodes with the clearest choice
+// are placed first), `rounds` times. Rounder subdomains have shorter
+// interfaces: on config 2 the block-Jacobi + coarse PCG needs 13-17% fewer
+// iterations and the largest halo shrinks from 98 to ~70 operand rows
+// (tools/partition_study.py). Subdomain numbers, and so the aggregates of
+// consecutive subdomains, are kept. Deterministic: fixed-order sums, index
+// tie-breaks. Within a subdomain the rows follow a Morton order of the node
+// positions, so consecutive rows (the dense preconditioner chunks) are compact.
+void lloyd_refine(const double* pos, const int* adj_off, const int* adj, const int* adj_cnt, int N, int G, int cap,
+                  int rounds, std::vector<int>& ids, std::vector<int>& leaf_begin) {
+    std::vector<int> label(N), fresh(N), count(G), order(N);
+    for (int g = 0; g < G; ++g)
+        for (int t = leaf_begin[g]; t < (g + 1 < G ? leaf_begin[g + 1] : N); ++t) label[ids[t]] = g;
+    constexpr int kCand = 8;  // candidate subdomains kept per node (own + neighbours'; more than 4-5 is rare)
+    std::vector<double> cen(3 * static_cast<size_t>(G)), cand_d(static_cast<size_t>(N) * kCand);
+    std::vector<int> cand(static_cast<size_t>(N) * kCand), ncand(N);
+    std::vector<int> bucket(1027), bkt(N);
+    for (int r = 0; r < rounds; ++r) {
+        std::fill(cen.begin(), cen.end(), 0.0);
+        std::fill(count.begin(), count.end(), 0);
+        for (int j = 0; j < N; ++j) {
+            double* cg = &cen[3 * static_cast<size_t>(label[j])];
+            cg[0] += pos[3 * j];
+            cg[1] += pos[3 * j + 1];
+            cg[2] += pos[3 * j + 2];
+            ++count[label[j]];
+        }
+        for (int g = 0; g < G; ++g) {
+            const double inv = 1.0 / std::max(1, count[g]);
+            for (int c = 0; c < 3; ++c) cen[3 * g + c] *= inv;
+        }
+        for (int j = 0; j < N; ++j) {
+            // candidate subdomains: own and the neighbours', nearest centroid first
+            int* cs = &cand[static_cast<size_t>(j) * kCand];
+            double* ds = &cand_d[static_cast<size_t>(j) * kCand];
+            int nc = 0;
+            cs[nc++] = label[j];
+            for (int t = adj_off[j], te = adj_off[j] + adj_cnt[j]; t < te; ++t) {
+                const int g = label[adj[t]];
+                bool seen = false;
+                for (int u = 0; u < nc; ++u) seen |= cs[u] == g;
+                if (!seen && nc < kCand) cs[nc++] = g;
+            }
+            const double px = pos[3 * j], py = pos[3 * j + 1], pz = pos[3 * j + 2];
+            for (int u = 0; u < nc; ++u) {
+                const double* cg = &cen[3 * static_cast<size_t>(cs[u])];
+                const double x = px - cg[0], y = py - cg[1], z = pz - cg[2];
+                ds[u] = x * x + y * y + z * z;
+            }
+            for (int u = 1; u < nc; ++u)  // insertion sort by (distance, subdomain)
+                for (int v = u; v > 0 && (ds[v] < ds[v - 1] || (ds[v] == ds[v - 1] && cs[v] < cs[v - 1])); --v) {
+                    std::swap(ds[v], ds[v - 1]);
+                    std::swap(cs[v], cs[v - 1]);
+                }
+            ncand[j] = nc;
+        }
+        // placement order: nodes with a single candidate first, then by the
+        // ratio of the nearest to the second nearest centroid distance in
+        // 1024 buckets (the clearest choices first; index order inside a
+        // bucket): a counting sort instead of a comparison sort
+        std::fill(bucket.begin(), bucket.end(), 0);
+        for (int j = 0; j < N; ++j) {
+            int b = 0;
+            if (ncand[j] > 1) {
+                const double d0 = cand_d[static_cast<size_t>(j) * kCand], d1 = cand_d[static_cast<size_t>(j) * kCand + 1];
+                b = 1 + (d1 > 0 ? std::min(1023, static_cast<int>(d0 / d1 * 1024.0)) : 1023);
+            }
+            bkt[j] = b;
+            ++bucket[b + 1];
+        }
+        for (int b = 0; b < 1025; ++b) bucket[b + 1] += bucket[b];
+        for (int j = 0; j < N; ++j) order[bucket[bkt[j]]++] = j;
+        std::fill(count.begin(), count.end(), 0);
+        int moved = 0;
+        for (int j : order) {
+            int pick = -1;
+            const int* cs = &cand[static_cast<size_t>(j) * kCand];
+            for (int t = 0; t < ncand[j] && pick < 0; ++t)
+                if (count[cs[t]] < cap) pick = cs[t];
+            if (pick < 0) {  // every candidate is full: the nearest subdomain with room
+                double best = 1e300;
+                for (int g = 0; g < G; ++g) {
+                    if (count[g] >= cap) continue;
+                    double d = 0;
+                    for (int c = 0; c < 3; ++c) {
+                        const double x = pos[3 * j + c] - cen[3 * g + c];
+                        d += x * x;
+                    }
+                    if (d < best) {
+                        best = d;
+                        pick = g;
+                    }
+                }
+            }
+            fresh[j] = pick;
+            moved += pick != label[j];
+            ++count[pick];
+        }
+        bool empty = false;
+        for (int g = 0; g < G; ++g) empty |= count[g] == 0;
+        if (empty) break;  // keep the previous round's subdomains
+        label.swap(fresh);
+        if (moved <= N / 256) break;  // converged: the last rounds move a handful of nodes
+    }
+    // rows: subdomain by subdomain, Morton order inside
+    std::fill(count.begin(), count.end(), 0);
+    for (int j = 0; j < N; ++j) ++count[label[j]];
+    leaf_begin[0] = 0;
+    for (int g = 0; g + 1 < G; ++g) leaf_begin[g + 1] = leaf_begin[g] + count[g];
+    std::vector<int> fill(leaf_begin.begin(), leaf_begin.begin() + G);
+    for (int j = 0; j < N; ++j) ids[fill[label[j]]++] = j;
+    std::vector<unsigned> code(N);
+    for (int g = 0; g < G; ++g) {
+        const int lo = leaf_begin[g], hi = lo + count[g];
+        double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+        for (int t = lo; t < hi; ++t)
+            for (int c = 0; c < 3; ++c) {
+                mn[c] = std::min(mn[c], pos[3 * ids[t] + c]);
+                mx[c] = std::max(mx[c], pos[3 * ids[t] + c]);
+            }
+        const double ext = std::max({mx[0] - mn[0], mx[1] - mn[1], mx[2] - mn[2], 1e-300});
+        for (int t = lo; t < hi; ++t) {
+            unsigned m = 0;
+            for (int c = 0; c < 3; ++c) {
+                unsigned q = static_cast<unsigned>(std::min(1023.0, (pos[3 * ids[t] + c] - mn[c]) / ext * 1023.0));
+                for (int b = 0; b < 10; ++b) m |= ((q >> b) & 1u) << (3 * b + c);
+            }
+            code[ids[t]] = m;
+        }
+        std::sort(ids.begin() + lo, ids.begin() + hi,
+                  [&](int x, int y) { return code[x] != code[y] ? code[x] < code[y] : x < y; });
+    }
+}
+
+void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit,
+                    const int* adj_off, const int* adj) {
     nodes = N;
     grid = std::max(1, std::min({num_sms, N, 32 * kMaxGridLoads}));
     const int cap_rows = (kPcgThreads * kMaxEpt) / 12;
@@ -1642,6 +1779,26 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
     RcbCtx ctx{node_pos, w.data(), &ids, &row_begin};
     rcb(ctx, 0, N, 0, grid);
     row_begin[grid] = N;
+    {
+        // Subdomains of one element per thread (<= 32 rows) are rounded; the
+        // cap keeps them there. Larger plans (several elements per thread,
+        // shared memory at its limit) keep the bisection.
+        int rcb_max = 0;
+        for (int g = 0; g < grid; ++g) rcb_max = std::max(rcb_max, row_begin[g + 1] - row_begin[g]);
+        int rounds = 16, cap_add = 10;
+        if (const char* e = std::getenv("NRR_LLOYD")) rounds = std::atoi(e);
+        if (const char* e = std::getenv("NRR_LLOYD_CAP")) cap_add = std::atoi(e);  // percent above the mean
+        const int cap_ept1 = kPcgThreads / 12;
+        if (adj_off != nullptr && rounds > 0 && grid > 1 && rcb_max <= cap_ept1) {
+            const int mean = (N + grid - 1) / grid;
+            // 10% above the mean measured best on config 2 (24 rows): 16 x 24
+            // subdomain-matvec tasks still fit one round of the CTA's 384
+            // threads; 25 rows cost +9% per PCG iteration (profiles/r04_lloyd_sweep.txt)
+            const int cap = std::min(cap_ept1, std::max(rcb_max, mean + (mean * cap_add + 99) / 100));
+            lloyd_refine(node_pos, adj_off, adj, row_nnz_by_node, N, grid, cap, rounds, ids, row_begin);
+            row_begin[grid] = N;
+        }
+    }
     row_node = ids;
     node_row.assign(N, 0);
     for (int r = 0; r < N; ++r) node_row[row_node[r]] = r;

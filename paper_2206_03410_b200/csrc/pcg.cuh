@@ -83,7 +83,10 @@ struct PcgPlan {
     std::vector<double> agg_center;  // n_agg*3
     std::vector<int> colx, ext_off, ext_node, ext_tl, touch_off, touch_agg;
     // partition + row order; row_nnz = blocks per node (for balance)
-    void build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit);
+    // adj_off / adj: the node graph (CSR by node id, self included; the first row_nnz_by_node[j] entries of
+    // row j are its distinct neighbours), used to round the subdomains after the bisection (pcg.cu)
+    void build(const double* node_pos, const int* row_nnz_by_node, int N, int num_sms, size_t smem_limit,
+               const int* adj_off = nullptr, const int* adj = nullptr);
     // smem sizing once the BSR (in solver-row order) is known
     void size_smem(const int* row_ptr_solver, const int* col, size_t smem_limit);
 };

@@ -575,7 +575,7 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     // solver row order: RCB subdomains, one per CTA (pcg.cu)
     clk.lap("pattern");
     const int sms = c->opt.max_ctas > 0 ? std::min(c->opt.max_ctas, c->num_sms) : c->num_sms;
-    if (N > 0) c->plan.build(p->node_positions, deg.data(), N, sms, c->smem_optin);
+    if (N > 0) c->plan.build(p->node_positions, deg.data(), N, sms, c->smem_optin, coff.data(), cflat.data());
     clk.lap("rcb plan");
     c->h_row_ptr.assign(N + 1, 0);
     c->h_col.clear();
