@@ -1780,21 +1780,24 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
     rcb(ctx, 0, N, 0, grid);
     row_begin[grid] = N;
     {
-        // Subdomains of one element per thread (<= 32 rows) are rounded; the
-        // cap keeps them there. Larger plans (several elements per thread,
-        // shared memory at its limit) keep the bisection.
+        // The subdomains are rounded with a size cap that keeps the plan's
+        // shape: the elements per thread of the bisection's largest
+        // subdomain, and (one element per thread) the 24 rows whose 16 x 24
+        // subdomain-matvec tasks still fit one round of the CTA's 384
+        // threads: 25 rows cost +9% per PCG iteration on config 2, 10% above
+        // the mean (24 rows there) measured best (profiles/r04_lloyd_sweep.txt).
         int rcb_max = 0;
         for (int g = 0; g < grid; ++g) rcb_max = std::max(rcb_max, row_begin[g + 1] - row_begin[g]);
         int rounds = 16, cap_add = 10;
         if (const char* e = std::getenv("NRR_LLOYD")) rounds = std::atoi(e);
         if (const char* e = std::getenv("NRR_LLOYD_CAP")) cap_add = std::atoi(e);  // percent above the mean
-        const int cap_ept1 = kPcgThreads / 12;
-        if (adj_off != nullptr && rounds > 0 && grid > 1 && rcb_max <= cap_ept1) {
+        int ept_rcb = 1;
+        while (rcb_max * 12 > ept_rcb * kPcgThreads) ept_rcb *= 2;
+        int bound = ept_rcb * kPcgThreads / 12;
+        if (rcb_max <= kPcgThreads / 16) bound = kPcgThreads / 16;
+        if (adj_off != nullptr && rounds > 0 && grid > 1) {
             const int mean = (N + grid - 1) / grid;
-            // 10% above the mean measured best on config 2 (24 rows): 16 x 24
-            // subdomain-matvec tasks still fit one round of the CTA's 384
-            // threads; 25 rows cost +9% per PCG iteration (profiles/r04_lloyd_sweep.txt)
-            const int cap = std::min(cap_ept1, std::max(rcb_max, mean + (mean * cap_add + 99) / 100));
+            const int cap = std::min(bound, std::max(rcb_max, mean + (mean * cap_add + 99) / 100));
             lloyd_refine(node_pos, adj_off, adj, row_nnz_by_node, N, grid, cap, rounds, ids, row_begin);
             row_begin[grid] = N;
         }
