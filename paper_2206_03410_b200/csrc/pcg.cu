@@ -846,7 +846,23 @@ __device__ __forceinline__ void iter_totals(const PcgArgs& a, const double* __re
     }
     double2 xa[4];
     const bool fast = a.use_coarse && a.agg_ctas == 8;
-    for (int o = threadIdx.x; a.use_coarse && o < nc * 3; o += blockDim.x) {
+    // 4 CTAs per aggregate: 32-byte aligned, zero padded; a thread's two
+    // outputs (o, o + blockDim) are loaded together
+    const bool fast4 = a.use_coarse && a.agg_ctas == 4 && nc * 3 <= 2 * static_cast<int>(blockDim.x);
+    if (fast4) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int o = threadIdx.x + h * blockDim.x;
+            xa[2 * h] = xa[2 * h + 1] = make_double2(0.0, 0.0);
+            if (o < nc * 3) {
+                const int g = o / 12, kc = o % 12;
+                const double2* src = reinterpret_cast<const double2*>(part + (7 + kc) * Gp + 4 * g);
+                xa[2 * h] = __ldcg(src);
+                xa[2 * h + 1] = __ldcg(src + 1);
+            }
+        }
+    }
+    for (int o = threadIdx.x; a.use_coarse && !fast4 && o < nc * 3; o += blockDim.x) {
         const int g = o / 12, kc = o % 12;
         const int c0 = g * a.agg_ctas, c1 = min(c0 + a.agg_ctas, G);
         const double* src = part + (7 + kc) * Gp + c0;
@@ -881,6 +897,13 @@ __device__ __forceinline__ void iter_totals(const PcgArgs& a, const double* __re
             s += xa[i].y;
         }
         ptq[threadIdx.x] = s;
+    }
+    if (fast4) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int o = threadIdx.x + h * blockDim.x;
+            if (o < nc * 3) ptq[o] = ((xa[2 * h].x + xa[2 * h].y) + xa[2 * h + 1].x) + xa[2 * h + 1].y;
+        }
     }
 }
 
@@ -1581,6 +1604,7 @@ struct RcbCtx {
     const int* weight;
     std::vector<int>* ids;
     std::vector<int>* leaf_begin;
+    int align = 1;  // splits of more than `align` leaves fall on a multiple of it: aggregates are subtrees
 };
 
 void rcb(RcbCtx& ctx, int lo, int hi, int g0, int g1) {
@@ -1589,7 +1613,14 @@ void rcb(RcbCtx& ctx, int lo, int hi, int g0, int g1) {
         (*ctx.leaf_begin)[g0] = lo;
         return;
     }
-    const int gm = (g0 + g1) / 2;
+    int gm = (g0 + g1) / 2;
+    if (ctx.align > 1 && g1 - g0 > ctx.align) {
+        // the multiple of `align` nearest the midpoint, strictly inside (g0, g1)
+        const int A = ctx.align;
+        gm = ((g0 + g1 + A) / (2 * A)) * A;
+        gm = std::max(gm, (g0 / A + 1) * A);
+        gm = std::min(gm, ((g1 - 1) / A) * A);
+    }
     double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
     for (int t = lo; t < hi; ++t)
         for (int c = 0; c < 3; ++c) {
@@ -1776,7 +1807,16 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
     if (const char* e = std::getenv("NRR_RCB_W")) wbase = std::atoi(e);
     for (int j = 0; j < N; ++j) w[j] = wbase + row_nnz_by_node[j];
     row_begin.assign(grid + 1, N);
+    // CTAs per coarse aggregate, decided before the bisection so that its
+    // splits fall on aggregate boundaries (an aggregate is then a subtree: a
+    // compact box, instead of 4 or 8 consecutive leaves that straddle
+    // subtrees). 4 CTAs per aggregate (37 aggregates on 148 CTAs): with
+    // aligned splits and rounded subdomains the offline count drops from 88
+    // (8 per aggregate) to 73 (tools/partition_study.py).
+    agg_ctas = std::max(4, (4 * grid + 159) / 160);
+    if (const char* e = std::getenv("NRR_AGG_CTAS")) agg_ctas = std::max((4 * grid + 159) / 160, std::atoi(e));
     RcbCtx ctx{node_pos, w.data(), &ids, &row_begin};
+    ctx.align = std::getenv("NRR_RCB_ALIGN") ? std::atoi(std::getenv("NRR_RCB_ALIGN")) : agg_ctas;
     rcb(ctx, 0, N, 0, grid);
     row_begin[grid] = N;
     {
@@ -1815,8 +1855,6 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
     // CTAs per coarse aggregate: 8 measured best on cfg2 (~20 nodes per CTA);
     // with large subdomains (cfg4, ~120 nodes per CTA) 4 (37 aggregates):
     // 298 -> 261 iterations, -8% per pass
-    agg_ctas = std::max(max_rows > 64 ? 4 : 8, (4 * grid + 159) / 160);
-    if (const char* e = std::getenv("NRR_AGG_CTAS")) agg_ctas = std::max((4 * grid + 159) / 160, std::atoi(e));
     if (const char* e = std::getenv("NRR_COARSE")) use_coarse = std::atoi(e) != 0;
     n_agg = (grid + agg_ctas - 1) / agg_ctas;
     node_agg.assign(N, 0);
