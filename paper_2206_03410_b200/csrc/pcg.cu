@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_partial_kernel(PcgArgs 
 // step costs one 4x4x4 product per tile instead of a shared-memory pass over
 // the matrix. Deterministic.
 constexpr int kCiThreads = 512;
-constexpr int kCiTiles = 2;  // n_agg^2 <= kCiThreads * kCiTiles  (n_agg <= 32)
+constexpr int kCiTiles = 3;  // n_agg^2 <= kCiThreads * kCiTiles  (n_agg <= 39: the 37 aggregates of 148 CTAs)
 __device__ __forceinline__ void mm4(const double* a, const double* b, double* c) {  // c = a b (row-major 4x4)
 #pragma unroll
     for (int r = 0; r < 4; ++r)
