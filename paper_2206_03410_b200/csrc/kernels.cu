@@ -252,7 +252,12 @@ __device__ __forceinline__ double transpose_reduce32(const double (&v)[32]) {
 // leaves slot l's total in lane l. Fixed order: deterministic; both mirrored
 // halves of an edge block are written from the same value (K bitwise
 // symmetric, robust_energy_tests.cpp:185-196).
-__global__ void __launch_bounds__(kAsmWarps * 32) assemble_kernel(DevProblem p, const double* __restrict__ wa,
+// three CTAs per SM (80 registers instead of 92, 16 B of spills): the kernel is latency-bound at 25%
+// occupancy; config 2 46.7 -> 37.4 us, config 4 289 -> 208 us (profiles/r04_occupancy_ab.txt)
+#ifndef NRR_ASM_MINB
+#define NRR_ASM_MINB 3
+#endif
+__global__ void __launch_bounds__(kAsmWarps * 32, NRR_ASM_MINB) assemble_kernel(DevProblem p, const double* __restrict__ wa,
                                                                   const double* __restrict__ q,
                                                                   const double* __restrict__ wr,
                                                                   const double* __restrict__ R, TermParams tp,

@@ -167,7 +167,12 @@ __device__ __forceinline__ float box_dist2(const float4& l, const float4& h, flo
     return dx * dx + dy * dy + dz * dz;
 }
 
-__global__ void __launch_bounds__(256) nn_kernel(BvhView bv, const double* __restrict__ queries, int nq,
+// five CTAs per SM (48 registers instead of 54, no spills): config 2 49.2 -> 46.5 us, config 4 538 -> 521 us;
+// six spill and lose (profiles/r04_occupancy_ab.txt)
+#ifndef NRR_NN_MINB
+#define NRR_NN_MINB 5
+#endif
+__global__ void __launch_bounds__(256, NRR_NN_MINB) nn_kernel(BvhView bv, const double* __restrict__ queries, int nq,
                                                   const int* __restrict__ prev_idx, int* __restrict__ out_idx,
                                                   double* __restrict__ out_d2, double* __restrict__ out_q,
                                                   const double* __restrict__ anchor) {
