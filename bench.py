@@ -57,8 +57,9 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--pcg-rtol", type=float, default=None, help="override the library default (1e-13)")
     ap.add_argument("--pairs", type=int, default=256, help="config 3: number of independent pairs")
-    ap.add_argument("--pair-streams", type=int, default=9,
-                    help="config 3: pairs run side by side per GPU (9: 7.5K vs 7.2K it/s at 6, profiles/r02_sweep_*)")
+    ap.add_argument("--pair-streams", type=int, default=12,
+                    help="config 3: pairs run side by side per GPU (12: 9.3K it/s; 6: 8.8K, 9: 9.1K, 18: 6.6K, "
+                         "profiles/r04_config3_streams_sweep.txt)")
     ap.add_argument("--pair-iters", type=int, default=50, help="config 3: MM iterations per pair")
     ap.add_argument("--pair-ctas", type=int, default=0,
                     help="config 3: PCG grid cap per pair (0 = SMs / pair-streams)")
