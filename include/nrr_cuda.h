@@ -284,6 +284,13 @@ int nrr_ctx_enable_timing(nrr_ctx* ctx, int32_t on);
  * calls): out8 = {ok, cluster size, max rows per CTA, max smem K blocks,
  * max ext rows, smem bytes, smem K blocks total, row entries read from L2} */
 int nrr_debug_solver_plan(const nrr_problem_view* p, int32_t num_sms, int64_t smem_limit, int64_t* out8);
+/* host-only probe of the PCG plan's partition (no device calls): the solver
+ * row order of the graph nodes and the subdomain (one CTA each) boundaries.
+ * out3 = {subdomains, CTAs per coarse aggregate, largest subdomain};
+ * row_begin has num_sms + 1 entries (the first out3[0] + 1 are written),
+ * row_node node_count entries. */
+int nrr_debug_pcg_partition(const nrr_problem_view* p, int32_t num_sms, int32_t* out3, int32_t* row_begin,
+                            int32_t* row_node);
 
 /* ---- setup (CPU; out of the hot path, the reference's setup API) ---- */
 /* edges_from_faces (surface.hpp:49-65); returns edge count, -1 on error */

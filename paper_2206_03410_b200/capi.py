@@ -133,6 +133,8 @@ _SIGS = {
     "nrr_ctx_comm_ms": (C.c_int, [C.c_void_p, f64p]),
     "nrr_ctx_enable_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "nrr_debug_solver_plan": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int64, C.POINTER(C.c_int64)]),
+    "nrr_debug_pcg_partition": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "nrr_edges_from_faces": (C.c_int, [i32p, C.c_int32, C.c_int32, i32p, C.c_int32, i32p]),
     "nrr_knn_edges": (C.c_int, [f64p, C.c_int32, C.c_int32, i32p, C.c_int32, i32p]),
     "nrr_avg_edge_length": (C.c_int, [f64p, C.c_int32, i32p, C.c_int32, f64p]),

@@ -2029,6 +2029,42 @@ int nrr_init_parameters(nrr_ctx* ctx, const nrr_solver_config* cfg, double* out6
     });
 }
 
+int nrr_debug_pcg_partition(const nrr_problem_view* p, int32_t num_sms, int32_t* out3, int32_t* row_begin,
+                            int32_t* row_node) {
+    return guarded([&] {
+        const int N = p->node_count, E = p->edge_count;
+        if (N <= 0 || num_sms <= 0) throw ConfigError("nrr_debug_pcg_partition: empty graph or no SMs");
+        // the node graph as set_problem builds it: CSR by node, self first, distinct neighbours in front
+        std::vector<int> coff(N + 1, 0);
+        for (int j = 0; j < N; ++j) coff[j + 1] = 1;
+        for (int e = 0; e < E; ++e) {
+            ++coff[p->edges[2 * e] + 1];
+            ++coff[p->edges[2 * e + 1] + 1];
+        }
+        for (int j = 0; j < N; ++j) coff[j + 1] += coff[j];
+        std::vector<int> cflat(coff[N]), cfill(coff.begin(), coff.end() - 1), deg(N);
+        for (int j = 0; j < N; ++j) cflat[cfill[j]++] = j;
+        for (int e = 0; e < E; ++e) {
+            const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
+            cflat[cfill[a]++] = b;
+            cflat[cfill[b]++] = a;
+        }
+        for (int j = 0; j < N; ++j) {
+            int* lo = cflat.data() + coff[j];
+            int* hi = cflat.data() + coff[j + 1];
+            std::sort(lo, hi);
+            deg[j] = static_cast<int>(std::unique(lo, hi) - lo);
+        }
+        PcgPlan plan;
+        plan.build(p->node_positions, deg.data(), N, num_sms, 0, coff.data(), cflat.data());
+        out3[0] = plan.grid;
+        out3[1] = plan.agg_ctas;
+        out3[2] = plan.max_rows;
+        for (int g = 0; g <= plan.grid; ++g) row_begin[g] = plan.row_begin[g];
+        for (int r = 0; r < N; ++r) row_node[r] = plan.row_node[r];
+    });
+}
+
 int nrr_debug_solver_plan(const nrr_problem_view* p, int32_t num_sms, int64_t smem_limit, int64_t* out8) {
     return guarded([&] {
         const int N = p->node_count, E = p->edge_count;
