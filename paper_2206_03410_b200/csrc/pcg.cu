@@ -2,27 +2,31 @@
 // solve_system :393-408) as a two-level preconditioned conjugate gradient in
 // FP64 on sm_100a.
 //
-// Layout. Graph nodes are partitioned by recursive coordinate bisection into
-// one compact subdomain per CTA (one CTA per SM). Each CTA copies its rows' K
-// blocks into shared memory once per solve, so every SpMV reads K from SMEM.
-// The three right-hand sides (output coordinates, energy.hpp:118-121) share
-// every K read; a thread owns (node, row r, column c) elements in registers.
+// Layout. Graph nodes are partitioned into one compact subdomain per CTA (one
+// CTA per SM): recursive coordinate bisection whose splits fall on coarse
+// aggregate boundaries, then a Lloyd relaxation that rounds the subdomains
+// (PcgPlan::build). Each CTA copies its rows' K blocks into shared memory once
+// per solve (when they fit), so every SpMV reads K from SMEM. The three
+// right-hand sides (output coordinates, energy.hpp:118-121) share every K
+// read; a thread owns (node, row r, column c) elements in registers.
 //
-// Preconditioner M^-1 = sum_j K_jj^-1 (4x4 block Jacobi; the north_star's
-// 12x12 per-node block is I3 (x) K_jj) + Psi K0^-1 Psi^T, a coarse correction
-// over aggregates of consecutive subdomains. Psi spans, per aggregate, the
-// 4 modes that make the regularizer vanish (a global affine map: node j's
-// unknowns [a; a.(p_j - c) + b], energy.hpp:77-84), so the graph-Laplacian-like
-// low modes that stall block Jacobi are solved exactly on the coarse level.
-// K0 = Psi^T K Psi (<= 160 x 160) is assembled per solve (CTA partials, fixed
-// order) and inverted by one CTA (Gauss-Jordan, SPD).
+// Preconditioner M^-1 = sum_k K_kk^-1 (subdomain block Jacobi: exact dense
+// inverses of the diagonal blocks of <= 32 consecutive rows, sub_invert_kernel)
+// + Psi K0^-1 Psi^T, a coarse correction over aggregates of 4 consecutive
+// subdomains. Psi spans, per aggregate, the 4 modes that make the regularizer
+// vanish (a global affine map: node j's unknowns [a; a.(p_j - c) + b],
+// energy.hpp:77-84), so the graph-Laplacian-like low modes that stall block
+// Jacobi are solved exactly on the coarse level. K0 = Psi^T K Psi (<= 160 x
+// 160) is assembled from CTA partials in a fixed order and inverted by one
+// CTA (Gauss-Jordan, SPD); both parts are reused across solves of a stage.
 //
-// Iteration (2 grid barriers, all reductions two-level and fixed-order so the
-// result is bitwise reproducible):
-//   A: q = K z + beta q, p = z + beta p; partials (p,q) and Psi^T q
-//   -- barrier --  alpha; rho -= alpha Psi^T q (coarse residual, replicated)
-//   B: x += alpha p, r -= alpha q, z = M_jj r + Psi K0^-1 rho; partials (r,z), max|r|
-//   -- barrier --  beta
+// Iteration: pipelined PCG (Ghysels & Vanroose) with ONE grid barrier; all
+// reductions are two-level and fixed-order, so the result is bitwise
+// reproducible. Before the barrier every CTA holds r, u = M r, w = K u for
+// its rows and publishes the partials of (r,u), (w,u), max|r|, Psi^T w and
+// m' = M_sub w; after it one L2 round trip brings the totals and the halo of
+// m', the coarse part is completed on own and halo rows, n = K m, and the
+// recurrences advance (see the loop in pcg_kernel).
 // Exit: the recursive residual reaches pcg_rtol*(1+|B|max); the true residual
 // B-KX must then meet the reference bar 1e-8*(1+|B|max) (energy.hpp:245),
 // otherwise PCG restarts from it. A 4x4 diagonal block whose Cholesky pivot
