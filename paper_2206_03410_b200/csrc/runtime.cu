@@ -512,6 +512,46 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
             uploader.err = std::current_exception();
         }
     });
+    // BSR pattern: diagonal + both halves of each edge (energy.hpp:264-279)
+    // flat CSR by counting (the node itself + both ends of every edge), then
+    // each row sorted and deduplicated
+    std::vector<int> coff(static_cast<size_t>(N) + 1, 0);
+    for (int j = 0; j < N; ++j) coff[j + 1] = 1;
+    for (int e = 0; e < E; ++e) {
+        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
+        if (a < 0 || b < 0 || a >= N || b >= N || a == b) throw ConfigError("graph edge index out of range");
+        ++coff[a + 1];
+        ++coff[b + 1];
+    }
+    for (int j = 0; j < N; ++j) coff[j + 1] += coff[j];
+    std::vector<int> cflat(coff[N]), cfill(coff.begin(), coff.end() - 1);
+    for (int j = 0; j < N; ++j) cflat[cfill[j]++] = j;
+    for (int e = 0; e < E; ++e) {
+        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
+        cflat[cfill[a]++] = b;
+        cflat[cfill[b]++] = a;
+    }
+    std::vector<int> deg(N);
+    for (int j = 0; j < N; ++j) {
+        int* lo = cflat.data() + coff[j];
+        int* hi = cflat.data() + coff[j + 1];
+        std::sort(lo, hi);
+        deg[j] = static_cast<int>(std::unique(lo, hi) - lo);
+    }
+    clk.lap("pattern");
+    // solver row order: bisection + relaxation, one subdomain per CTA (pcg.cu),
+    // on a helper thread beside the influence validation below (it only
+    // needs the node graph)
+    const int sms = c->opt.max_ctas > 0 ? std::min(c->opt.max_ctas, c->num_sms) : c->num_sms;
+    Joiner planner;
+    if (N > 0)
+        planner.t = std::thread([c, p, N, sms, &deg, &coff, &cflat, &planner] {
+            try {
+                c->plan.build(p->node_positions, deg.data(), N, sms, c->smem_optin, coff.data(), cflat.data());
+            } catch (...) {
+                planner.err = std::current_exception();
+            }
+        });
     // influence validation (the constants w [v - p; 1] and sum w p are built
     // on the device, setup_gpu.cu); entries per vertex for the contributor lists
     std::vector<long long> pair_off(static_cast<size_t>(n) + 1, 0);
@@ -546,37 +586,8 @@ void set_problem(nrr_ctx* c, const nrr_problem_view* p) {
     const long long entries = pair_off[n];
     if (entries >= (1LL << 31)) throw ConfigError("assembly contributor lists exceed 2^31 entries");
     clk.lap("influence constants");
-    // BSR pattern: diagonal + both halves of each edge (energy.hpp:264-279)
-    // flat CSR by counting (the node itself + both ends of every edge), then
-    // each row sorted and deduplicated
-    std::vector<int> coff(static_cast<size_t>(N) + 1, 0);
-    for (int j = 0; j < N; ++j) coff[j + 1] = 1;
-    for (int e = 0; e < E; ++e) {
-        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
-        if (a < 0 || b < 0 || a >= N || b >= N || a == b) throw ConfigError("graph edge index out of range");
-        ++coff[a + 1];
-        ++coff[b + 1];
-    }
-    for (int j = 0; j < N; ++j) coff[j + 1] += coff[j];
-    std::vector<int> cflat(coff[N]), cfill(coff.begin(), coff.end() - 1);
-    for (int j = 0; j < N; ++j) cflat[cfill[j]++] = j;
-    for (int e = 0; e < E; ++e) {
-        const int a = p->edges[2 * e], b = p->edges[2 * e + 1];
-        cflat[cfill[a]++] = b;
-        cflat[cfill[b]++] = a;
-    }
-    std::vector<int> deg(N);
-    for (int j = 0; j < N; ++j) {
-        int* lo = cflat.data() + coff[j];
-        int* hi = cflat.data() + coff[j + 1];
-        std::sort(lo, hi);
-        deg[j] = static_cast<int>(std::unique(lo, hi) - lo);
-    }
-    // solver row order: RCB subdomains, one per CTA (pcg.cu)
-    clk.lap("pattern");
-    const int sms = c->opt.max_ctas > 0 ? std::min(c->opt.max_ctas, c->num_sms) : c->num_sms;
-    if (N > 0) c->plan.build(p->node_positions, deg.data(), N, sms, c->smem_optin, coff.data(), cflat.data());
-    clk.lap("rcb plan");
+    planner.join();  // solver row order (started above)
+    clk.lap("rcb plan (rest)");
     c->h_row_ptr.assign(N + 1, 0);
     c->h_col.clear();
     for (int r = 0; r < N; ++r) {
