@@ -76,6 +76,9 @@ class Dist:
         if self.world > 1:
             import torch
             import torch.distributed as dist
+            if self.local >= torch.cuda.device_count():
+                raise SystemExit("bench.py: rank %d needs GPU %d but only %d are visible (one process per GPU)"
+                                 % (self.rank, self.local, torch.cuda.device_count()))
             torch.cuda.set_device(self.local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.torch, self.dist = torch, dist
