@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(kPcgThreads, 1) pcg_kernel(PcgArgs a_param) {
         sh.offx = p;
         p += 3 * static_cast<size_t>(a.max_ext);
         sh.cinv = p;
-        p += 4 * static_cast<size_t>(a.max_touch) * nc;
+        if (a.use_coarse) p += 4 * static_cast<size_t>(a.max_touch) * nc;  // as PcgPlan::size_smem
         sh.yt = p;
         p += 12 * a.max_touch;
         sh.ptq = p;

@@ -454,6 +454,36 @@ def test_step_parity_large_subdomains(cap):
         c.close()
 
 
+@pytest.mark.parametrize("env", [{"NRR_LLOYD": "0"}, {"NRR_AGG_CTAS": "8"}, {"NRR_RCB_ALIGN": "1"},
+                                 {"NRR_LLOYD": "3", "NRR_LLOYD_CAP": "30"}, {"NRR_COARSE": "0"}])
+@pytest.mark.parametrize("cap", [0, 10])
+def test_step_parity_plan_variants(monkeypatch, env, cap):
+    """The plan knobs (bisection only, 8 CTAs per aggregate, unaligned splits,
+    a loose size cap, no coarse space) change the preconditioner, never the
+    solution: the same teacher-forced pass meets the reference bar on a full
+    grid (rounded 1-element-per-thread subdomains) and on a 10-CTA grid."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = R.make_problem(1, scale=0.4)
+    c = R.Context(max_ctas=cap) if cap else R.Context()
+    try:
+        c.set_problem(p)
+        c.set_target(p.target)
+        N = p.graph.node_count
+        row_ptr, _ = R.bsr_pattern(p.graph)
+        nnzb = int(row_ptr[-1])
+        X = random_transforms(N, 11, 0.1)
+        prm = (0.8, 1.7, 0.09, 0.12)
+        g = c.step(X, prm, nnzb=nnzb)
+        o = O.step(p, X, prm, nnzb)
+        assert np.array_equal(g["index"], o["index"])
+        assert np.allclose(g["energy"], o["energy"], rtol=1e-12, atol=0)
+        err = np.max(np.abs(g["Xmm"] - o["Xmm"]))
+        assert err <= 1e-8 * (1 + np.max(np.abs(o["Xmm"]))), err
+    finally:
+        c.close()
+
+
 def test_cluster_resident_pcg_step_parity(monkeypatch, strip):
     """The opt-in cluster-resident solver (NRR_PCG=cluster: one thread-block
     cluster, K in distributed shared memory) solves the same teacher-forced
