@@ -1807,7 +1807,11 @@ void PcgPlan::build(const double* node_pos, const int* row_nnz_by_node, int N, i
         throw ConfigError("PCG: deformation graph too large for one cooperative grid (nodes per SM > 256)");
     std::vector<int> ids(N), w(N);
     std::iota(ids.begin(), ids.end(), 0);
-    int wbase = 6;  // RCB cost per node: wbase + its block count (6 measured best on cfg2)
+    // bisection cost per node: wbase + its block count. With the relaxation on
+    // top a near count-balanced bisection is the better start (config 2:
+    // 1,170 it/s at 6, 1,208 at 30, 1,232 at 100, profiles/r04_rcb_weight_sweep.txt;
+    // 6 had measured best for the bisection alone)
+    int wbase = 100;
     if (const char* e = std::getenv("NRR_RCB_W")) wbase = std::atoi(e);
     for (int j = 0; j < N; ++j) w[j] = wbase + row_nnz_by_node[j];
     row_begin.assign(grid + 1, N);
