@@ -1728,7 +1728,8 @@ void lloyd_refine(const double* pos, const int* adj_off, const int* adj, const i
             int b = 0;
             if (ncand[j] > 1) {
                 const double d0 = cand_d[static_cast<size_t>(j) * kCand], d1 = cand_d[static_cast<size_t>(j) * kCand + 1];
-                b = 1 + (d1 > 0 ? std::min(1023, static_cast<int>(d0 / d1 * 1024.0)) : 1023);
+                const double ratio = d0 / d1;  // in [0, 1]; anything else (0/0, non-finite positions) goes last
+                b = (ratio >= 0.0 && ratio < 1.0) ? 1 + static_cast<int>(ratio * 1024.0) : 1024;
             }
             bkt[j] = b;
             ++bucket[b + 1];
